@@ -1,0 +1,341 @@
+"""Benchmark of the north-star workload: the 3D complex128 μ-mode exponential step at n=256^3.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One "step" = one exact propagator step ``u <- u x_1 E_1 x_2 E_2 x_3 E_3`` of a
+256^3 complex128 tensor (E_mu = expm(0.01 i D2), D2 the periodic p=2 second
+difference on [0, 2π)), i.e. 103.08 GFLOP at 8 flop per
+complex multiply-add.  Prints ONE JSON line (rank 0).
+
+* value      — steps/s of the whole job, device-resident inputs, CUDA events
+               around exactly K steps, max over ranks.
+* e2e        — the same metric through the public drop-in call
+               ``km.step(cache, u_host)`` with a pinned host array in and a host
+               array out (H2D + D2H inside the timed region).
+* roofline   — the dominant kernel (mumode_kernel, DMMA) achieved TFLOP/s vs
+               the measured FP64 tensor-core peak (profiles/fp64_peak.json).
+* cpu_baseline — the reference algorithm (oracle/ numpy restatement, same
+               numpy.matmul calls as tensor.py:124-139) on the host cores.
+
+The state (268 MB) exceeds the 126 MB L2, so no flush is needed between steps.
+Multi-GPU (torchrun, N>1): the 256^3 state is split into slabs along
+direction 3 (strong scaling); see paper_2103_01691_b200/dist.py.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N = 256
+TAU = 0.01
+FLOP_PER_STEP = 8 * 3 * N**4  # 8 flop per complex MAC, 3 directions, N^3 * n MACs each
+METRIC = "3D μ-mode step/s & GFLOP/s (complex128, n=256³) at 1/2/4/8 B200 vs CPU ref"
+WORKLOAD = {
+    "workload": "schrodinger3d_free_step_c128_n256",
+    "n": N,
+    "tau": TAU,
+    "factors": "E_mu = expm(i*tau*D2), D2 periodic 2nd-order on [0,2pi) (host scipy)",
+    "state_bytes": 16 * N**3,
+    "l2": "state 268 MB > 126 MB L2; no flush needed",
+    "flop_per_step": FLOP_PER_STEP,
+}
+PROFILES = os.path.join(ROOT, "profiles")
+
+
+def build_inputs():
+    import paper_2103_01691_b200 as km
+
+    rng = np.random.default_rng(0)
+    u = np.asfortranarray(rng.standard_normal((N,) * 3) + 1j * rng.standard_normal((N,) * 3))
+    d2 = km.heat_factors(N, 2).factors[0]
+    cache = km.prepare(km.KroneckerOp((1j * d2,) * 3), TAU)
+    return u, cache
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.15)
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[4:8]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def fp64_peak():
+    path = os.path.join(PROFILES, "fp64_peak.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["dmma_tflops_sustained"]), p.get("source", path)
+    except (OSError, KeyError, ValueError):
+        return 37.1, "fallback: DMMA.8x8x4 microbenchmark burst (tools/fp64_peak.cu), not committed"
+
+
+def traffic_from_profile():
+    path = os.path.join(PROFILES, "ncu_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_reference(u, cache, budget_s, max_steps):
+    """The reference algorithm (oracle numpy restatement) on all host threads."""
+    from threadpoolctl import threadpool_info, threadpool_limits
+
+    from oracle import kronmode_oracle as orc
+
+    cores = os.cpu_count() or 1
+    with threadpool_limits(limits=cores):
+        blas = [f"{i.get('internal_api')} {i.get('version')} x{i.get('num_threads')}" for i in threadpool_info()]
+        orc.step(cache.exps, u)  # warm-up
+        times = []
+        v = u
+        t_start = time.perf_counter()
+        while len(times) < max_steps:
+            t0 = time.perf_counter()
+            v = orc.step(cache.exps, v)
+            times.append(time.perf_counter() - t0)
+            if time.perf_counter() - t_start > budget_s:
+                break
+    sps = len(times) / sum(times)
+    return {
+        "value": sps,
+        "unit": "steps/s",
+        "cores": cores,
+        "kind": "port",
+        "sample": f"{len(times)} full 256^3 c128 steps after 1 warm-up, numpy.matmul ({'; '.join(blas)})",
+        "gflops": sps * FLOP_PER_STEP / 1e9,
+        "ms_per_step": 1e3 / sps,
+    }
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    u, cache = build_inputs()
+    steps = max(1, args.steps)
+    # bounded: at most ~120 s of CPU work whatever K is
+    cb = cpu_reference(u, cache, budget_s=120.0, max_steps=steps)
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": cb["value"],
+        "unit": "steps/s",
+        "n_gpus": args.gpus,
+        "steps": steps,
+        "warmup": args.warmup,
+        "ms_per_step": cb["ms_per_step"],
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "complex128",
+        "data": "synthetic (seeded normal complex tensor)",
+        "config": dict(WORKLOAD),
+        "gflops": cb["gflops"],
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2103_01691_b200 as km
+    from paper_2103_01691_b200 import _device as dv
+    from paper_2103_01691_b200 import dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as tdist
+
+        tdist.init_process_group("nccl", device_id=dev)
+
+    u_host, cache = build_inputs()
+    stream = torch.cuda.current_stream(dev)
+
+    if world == 1:
+        state = dv.to_device(u_host, np.complex128, dev)
+        mats = cache.device_exps((np.complex128,) * 3, dev)
+        runner = dist.LocalStepper(state, mats)
+    else:
+        runner = dist.SlabStepper.from_global(u_host, cache, dev)
+
+    for _ in range(max(args.warmup, 3)):
+        runner.step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as tdist
+
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            runner.step()
+        stop.record(stream)
+        barrier()
+    ms = start.elapsed_time(stop)
+    if world > 1:
+        import torch.distributed as tdist
+
+        t = torch.tensor([ms], device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = 1e3 / ms_per_step  # whole job: one global 256^3 step per step
+
+    # per-launch roofline of the dominant kernel (single GPU timing of one step's launches)
+    roof = None
+    if rank == 0:
+        per_mode = runner.time_launches(reps=10) if world == 1 else None
+        peak, peak_src = fp64_peak()
+        if per_mode:
+            flop_launch = 8 * N**4
+            avg_ms = sum(per_mode) / len(per_mode)
+            achieved = flop_launch / (avg_ms * 1e-3) / 1e12
+            roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": traffic_from_profile(),
+                    "kernel": "mumode_kernel (DMMA.8x8x4, complex128)",
+                    "algorithmic_per_launch": f"{flop_launch} flop (8 * 256^4)",
+                    "launch_ms": per_mode, "peak_source": peak_src}
+
+    # e2e through the public drop-in call with host buffers
+    e2e = None
+    if world == 1:
+        pinned = torch.empty((N, N, N), dtype=torch.complex128, pin_memory=True)
+        pinned_np = pinned.numpy()
+        pinned_np[...] = u_host.transpose(2, 1, 0)  # C-order buffer ...
+        host_in = pinned_np.transpose(2, 1, 0)      # ... viewed column-major, same memory
+        assert host_in.flags.f_contiguous
+        e2e_steps = max(3, min(args.steps, 20))
+        out = km.step(cache, host_in)  # warm-up (pinned-memory path, allocator warm)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            out = km.step(cache, host_in)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        e2e = {"value": e2e_steps / el, "unit": "steps/s", "h2d_bytes_per_step": int(host_in.nbytes),
+               "d2h_bytes_per_step": int(out.nbytes), "steps": e2e_steps,
+               "call": "paper_2103_01691_b200.step(cache, numpy F-array in pinned memory) -> numpy"}
+
+    if rank == 0:
+        cb = cpu_reference(u_host, cache, budget_s=20.0, max_steps=50) if (world == 1 and not args.no_cpu) else None
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "steps/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": max(args.warmup, 3),
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "complex128",
+            "data": "synthetic (seeded normal complex tensor, host-built expm factors)",
+            "config": dict(WORKLOAD, parallelism=("single GPU" if world == 1 else f"slab{world} along direction 3")),
+            "gflops": value * FLOP_PER_STEP / 1e9,
+            "roofline": roof,
+            "cpu_baseline": cb,
+            "e2e": e2e,
+            "clocks": clocks.summary(),
+            "gpu_launches": runner.launches_per_step * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as tdist
+
+        tdist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,117 @@
+/*
+ * kmb200.h — C ABI of the B200 μ-mode hot path (libkmb200.so).
+ *
+ * The reference (`kronmode` 0.1.0, /root/reference/pkg/src/kronmode) is pure
+ * Python on numpy; its hot path has no FFI of its own — every product ends in
+ * `np.matmul` (tensor.py:129, tensor.py:139).  This header is the boundary a
+ * host binding crosses instead: plain device pointers, sizes and a stream, no
+ * torch or numpy types.  The Python mirror in `paper_2103_01691_b200/` binds it
+ * with ctypes (see INTEGRATION.md for the binding a kronmode maintainer would
+ * add).
+ *
+ * Conventions (all entry points):
+ *   - Tensors are column-major (direction 1 fastest), as tensor.py:3-6.
+ *   - Matrices L (m x n_mu) are row-major (C order), as numpy hands them over.
+ *   - All pointers are DEVICE pointers; the library never allocates, never
+ *     synchronises the host and launches only on `stream` (a cudaStream_t,
+ *     NULL = legacy default stream).
+ *   - Return value 0 on success, KM_EINVAL for a rejected argument, KM_ECUDA
+ *     for a CUDA launch/runtime failure; km_last_error() gives the message of
+ *     the last failure on the calling thread.
+ *   - Shapes and directions are validated by the host mirror first so that
+ *     its exceptions match the reference's messages (tensor.py:62-66,
+ *     102-111, 151-161); the C side re-checks only what would fault.
+ */
+#ifndef KMB200_H
+#define KMB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KMB200_ABI_VERSION 1
+#define KM_MAX_D 8
+
+/* element types; complex values are interleaved (re, im) pairs */
+enum km_dtype { KM_F32 = 0, KM_F64 = 1, KM_C64 = 2, KM_C128 = 3 };
+
+enum km_status { KM_OK = 0, KM_EINVAL = 1, KM_ECUDA = 2 };
+
+/* pointwise operators that can be fused into a product epilogue (post) or
+ * applied as a standalone pass (pre) */
+enum km_op_kind {
+  KM_OP_NONE = 0,
+  /* Gross–Pitaevskii nonlinear half-step, problems.py:542-545:
+   *   psi <- psi * exp(i * coef * (1 - |psi|^2 / (w_1[i_1] * ... * w_d[i_d])))
+   * with coef = 0.5 * half_tau; `weights[mu]` are device f64 vectors. */
+  KM_OP_GPE_PHASE = 1,
+  /* multiplication by a complex factor that depends on one direction only:
+   *   psi <- psi * diag[i_{diag_dir}]     (diag: device c128 vector)
+   * used for the time-dependent potential phase exp(-i x_3 ∫ sin^2). */
+  KM_OP_DIAG = 2
+};
+
+typedef struct km_pointop {
+  int32_t kind;                       /* enum km_op_kind */
+  int32_t d;                          /* tensor order */
+  int64_t dims[KM_MAX_D];             /* extents of the tensor the op sees */
+  const double* weights[KM_MAX_D];    /* KM_OP_GPE_PHASE */
+  double coef;                        /* KM_OP_GPE_PHASE */
+  const void* diag;                   /* KM_OP_DIAG, c128 vector of dims[diag_dir] */
+  int32_t diag_dir;                   /* KM_OP_DIAG, 0-based direction */
+  int32_t pad_;
+} km_pointop;
+
+/* ABI version and build info */
+int km_abi_version(void);
+const char* km_build_info(void);
+const char* km_last_error(void);
+
+/*
+ * μ-mode product, out = u ×_μ L  (reference: tensor.mu_mode_product,
+ * tensor.py:80-140).  The tensor is flattened to (n_left, n_mu, n_right)
+ * exactly as tensor.py:132-134 does; n_left == 1 is the reference's μ=1 branch
+ * (tensor.py:124-130).  `out` has shape (n_left, m, n_right).
+ *
+ * u_dtype / L_dtype must be of one precision (F32/C64 or F64/C128); the
+ * result is complex if either operand is.  `post` (may be NULL) is fused into
+ * the epilogue and sees the output tensor with extents post->dims.
+ * u and out must not overlap.
+ */
+int km_mumode(const void* u, int u_dtype, const void* L, int L_dtype, void* out,
+              int64_t m, int64_t n_left, int64_t n_mu, int64_t n_right,
+              const km_pointop* post, void* stream);
+
+/*
+ * Tucker operator / exact propagator step (reference: tensor.tucker,
+ * tensor.py:143-166; kron.step, kron.py:110-121; the Strang composition
+ * problems.py:548-565 when pre/post are phases).
+ *
+ *   out = post( pre(u) ×_1 mats[0] ×_2 ... ×_d mats[d-1] )
+ *
+ * mats[mu] == NULL skips that direction (tensor.py:164-165).  mats[mu] has
+ * rows[mu] rows and dims[mu] columns.  ws0/ws1 are scratch buffers, each at
+ * least the byte size of the largest intermediate (km_tucker_workspace()).
+ * pre is applied in a standalone pass, post is fused into the last product.
+ */
+int km_tucker(const void* u, int u_dtype, int d, const int64_t* dims,
+              const void* const* mats, const int* mat_dtypes, const int64_t* rows,
+              void* out, void* ws0, void* ws1,
+              const km_pointop* pre, const km_pointop* post, void* stream);
+
+/* bytes each of ws0/ws1 needs for km_tucker with these arguments */
+int km_tucker_workspace(int u_dtype, int d, const int64_t* dims, const void* const* mats,
+                        const int* mat_dtypes, const int64_t* rows, size_t* bytes);
+
+/* standalone pointwise operator, out = op(in) over n elements of a complex
+ * tensor (dtype KM_C64 or KM_C128); in == out is allowed */
+int km_pointwise(const void* in, void* out, int dtype, int64_t n, const km_pointop* op,
+                 void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KMB200_H */

@@ -1,0 +1,184 @@
+"""Device-side plumbing: column-major torch tensors, dtype codes, streams.
+
+PyTorch is used only for device memory, streams and copies.  Tensors keep the
+reference's column-major layout (tensor.py:3-6): a state of shape
+(n_1, ..., n_d) is a torch tensor with strides (1, n_1, n_1*n_2, ...).  Never
+call ``.contiguous()`` on a state — that would silently reorder it to C order.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .errors import DeviceError
+
+try:
+    import torch
+except ImportError:  # pragma: no cover - torch is part of the image
+    torch = None
+
+_NP_TO_CODE = {
+    np.dtype(np.float32): _native.KM_F32,
+    np.dtype(np.float64): _native.KM_F64,
+    np.dtype(np.complex64): _native.KM_C64,
+    np.dtype(np.complex128): _native.KM_C128,
+}
+SUPPORTED = tuple(_NP_TO_CODE)
+
+
+def torch_dtype(np_dtype):
+    return {
+        np.dtype(np.float32): torch.float32,
+        np.dtype(np.float64): torch.float64,
+        np.dtype(np.complex64): torch.complex64,
+        np.dtype(np.complex128): torch.complex128,
+    }[np.dtype(np_dtype)]
+
+
+def np_dtype(t_dtype):
+    return {
+        torch.float32: np.dtype(np.float32),
+        torch.float64: np.dtype(np.float64),
+        torch.complex64: np.dtype(np.complex64),
+        torch.complex128: np.dtype(np.complex128),
+        torch.float16: np.dtype(np.float16),
+        torch.int64: np.dtype(np.int64),
+        torch.int32: np.dtype(np.int32),
+        torch.bool: np.dtype(np.bool_),
+    }[t_dtype]
+
+
+def code(np_dt):
+    return _NP_TO_CODE[np.dtype(np_dt)]
+
+
+def is_tensor(x):
+    return torch is not None and isinstance(x, torch.Tensor)
+
+
+def device():
+    """The CUDA device used for host (numpy) inputs; raises without a GPU."""
+    if torch is None or not torch.cuda.is_available():
+        raise DeviceError("no CUDA device is available (this package has no CPU path)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr(dev=None):
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def f_strides(shape):
+    strides, s = [], 1
+    for n in shape:
+        strides.append(s)
+        s *= int(n)
+    return tuple(strides)
+
+
+def is_fortran(t):
+    """Column-major dense (size-1 extents may carry any stride)."""
+    s = 1
+    for n, st in zip(t.shape, t.stride()):
+        if n != 1 and st != s:
+            return False
+        s *= n
+    return True
+
+
+def fortran_empty(shape, dtype, dev):
+    """Uninitialised column-major device tensor of the given shape."""
+    shape = tuple(int(n) for n in shape)
+    if not shape:
+        return torch.empty((), dtype=dtype, device=dev)
+    return torch.empty(tuple(reversed(shape)), dtype=dtype, device=dev).permute(
+        *reversed(range(len(shape)))
+    )
+
+
+def as_fortran(t):
+    """``t`` itself when already column-major, else a column-major copy."""
+    if is_fortran(t):
+        return t
+    out = fortran_empty(t.shape, t.dtype, t.device)
+    out.copy_(t)
+    return out
+
+
+def to_device(a, dtype, dev):
+    """numpy array → column-major device tensor of ``dtype`` (numpy dtype).
+
+    A page-locked source (e.g. a view of ``torch.empty(..., pin_memory=True)``)
+    is copied with an asynchronous DMA on the current stream.
+    """
+    a = np.asarray(a)
+    if a.dtype != dtype:
+        a = a.astype(dtype, order="F")
+    a = np.asfortranarray(a)
+    if a.ndim == 0:
+        return torch.tensor(a.item(), dtype=torch_dtype(dtype), device=dev)
+    host = torch.from_numpy(a)  # keeps the F strides, shares memory
+    out = fortran_empty(a.shape, torch_dtype(dtype), dev)
+    out.copy_(host, non_blocking=a.nbytes >= _PINNED_MIN and host.is_pinned())
+    return out
+
+
+def tensor_as(t, dtype):
+    """Device tensor converted to numpy ``dtype``, keeping column-major strides."""
+    td = torch_dtype(dtype)
+    if t.dtype == td:
+        return as_fortran(t)
+    out = fortran_empty(t.shape, td, t.device)
+    out.copy_(t)
+    return out
+
+
+def matrix_to_device(m, dtype, dev):
+    """Small matrix → C-contiguous (row-major) device tensor, as the C ABI wants."""
+    if is_tensor(m):
+        return m.to(device=dev, dtype=torch_dtype(dtype)).contiguous()
+    m = np.ascontiguousarray(np.asarray(m), dtype=dtype)
+    return torch.from_numpy(m).to(dev)
+
+
+_PINNED_MIN = 1 << 20
+
+
+def to_host(t):
+    """Device tensor → numpy array with the same (column-major) layout.
+
+    Large results land in page-locked memory (torch's caching host allocator)
+    so the device→host copy runs at DMA speed; the returned array keeps that
+    buffer alive.
+    """
+    t = t.detach()
+    if t.is_cuda and t.numel() * t.element_size() >= _PINNED_MIN and is_fortran(t):
+        shape = tuple(t.shape)
+        host = torch.empty(tuple(reversed(shape)), dtype=t.dtype, pin_memory=True).permute(
+            *reversed(range(len(shape))))
+        host.copy_(t, non_blocking=True)
+        torch.cuda.current_stream(t.device).synchronize()
+        return host.numpy()
+    return t.cpu().numpy()
+
+
+_VEC_CACHE = {}
+_VEC_CACHE_MAX = 64
+
+
+def cached_vector(v, dtype, dev):
+    """Device copy of a small host vector/matrix, memoised by content."""
+    if is_tensor(v):
+        return v.to(device=dev, dtype=torch_dtype(dtype)).contiguous()
+    arr = np.ascontiguousarray(np.asarray(v), dtype=dtype)
+    key = (str(dev), arr.dtype.str, arr.shape, arr.tobytes())
+    hit = _VEC_CACHE.get(key)
+    if hit is not None:
+        return hit
+    t = torch.from_numpy(arr).to(dev)
+    if len(_VEC_CACHE) >= _VEC_CACHE_MAX:
+        _VEC_CACHE.pop(next(iter(_VEC_CACHE)))
+    _VEC_CACHE[key] = t
+    return t

@@ -1,0 +1,116 @@
+"""ctypes binding of ``libkmb200.so`` (the C ABI declared in include/kmb200.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` (or ``make -C
+paper_2103_01691_b200/csrc``).  There is no CPU fallback: every public entry
+point that computes goes through :func:`lib`, which raises
+:class:`NativeLibraryError` when the shared object is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import ConfigurationError, DeviceError, NativeLibraryError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libkmb200.so")
+ABI_VERSION = 1
+MAX_D = 8
+
+KM_F32, KM_F64, KM_C64, KM_C128 = 0, 1, 2, 3
+KM_OK, KM_EINVAL, KM_ECUDA = 0, 1, 2
+OP_NONE, OP_GPE_PHASE, OP_DIAG = 0, 1, 2
+
+# every symbol include/kmb200.h declares
+EXPORTS = (
+    "km_abi_version",
+    "km_build_info",
+    "km_last_error",
+    "km_mumode",
+    "km_tucker",
+    "km_tucker_workspace",
+    "km_pointwise",
+)
+
+
+class PointOp(ctypes.Structure):
+    """Mirror of ``km_pointop`` (include/kmb200.h)."""
+
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("d", ctypes.c_int32),
+        ("dims", ctypes.c_int64 * MAX_D),
+        ("weights", ctypes.c_void_p * MAX_D),
+        ("coef", ctypes.c_double),
+        ("diag", ctypes.c_void_p),
+        ("diag_dir", ctypes.c_int32),
+        ("pad_", ctypes.c_int32),
+    ]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def _declare(lib):
+    c_int, c_i64, c_vp, c_sz = ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t
+    p_op = ctypes.POINTER(PointOp)
+    lib.km_abi_version.restype = c_int
+    lib.km_abi_version.argtypes = []
+    lib.km_build_info.restype = ctypes.c_char_p
+    lib.km_build_info.argtypes = []
+    lib.km_last_error.restype = ctypes.c_char_p
+    lib.km_last_error.argtypes = []
+    lib.km_mumode.restype = c_int
+    lib.km_mumode.argtypes = [c_vp, c_int, c_vp, c_int, c_vp, c_i64, c_i64, c_i64, c_i64, p_op, c_vp]
+    lib.km_tucker.restype = c_int
+    lib.km_tucker.argtypes = [
+        c_vp, c_int, c_int, ctypes.POINTER(c_i64), ctypes.POINTER(c_vp), ctypes.POINTER(c_int),
+        ctypes.POINTER(c_i64), c_vp, c_vp, c_vp, p_op, p_op, c_vp,
+    ]
+    lib.km_tucker_workspace.restype = c_int
+    lib.km_tucker_workspace.argtypes = [
+        c_int, c_int, ctypes.POINTER(c_i64), ctypes.POINTER(c_vp), ctypes.POINTER(c_int),
+        ctypes.POINTER(c_i64), ctypes.POINTER(c_sz),
+    ]
+    lib.km_pointwise.restype = c_int
+    lib.km_pointwise.argtypes = [c_vp, c_vp, c_int, c_i64, p_op, c_vp]
+
+
+def lib():
+    """The loaded library (loads on first use; raises if it is missing)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise NativeLibraryError(
+                    f"{LIB_PATH} is missing; build it with "
+                    "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)"
+                )
+            try:
+                handle = ctypes.CDLL(LIB_PATH)
+            except OSError as exc:
+                raise NativeLibraryError(f"cannot load {LIB_PATH}: {exc}") from exc
+            missing = [s for s in EXPORTS if not hasattr(handle, s)]
+            if missing:
+                raise NativeLibraryError(f"{LIB_PATH} lacks symbols {missing}; rebuild it")
+            _declare(handle)
+            if handle.km_abi_version() != ABI_VERSION:
+                raise NativeLibraryError(
+                    f"{LIB_PATH} has ABI {handle.km_abi_version()}, expected {ABI_VERSION}; rebuild it"
+                )
+            _lib = handle
+    return _lib
+
+
+def check(rc):
+    """Map a C status code to the exception hierarchy."""
+    if rc == KM_OK:
+        return
+    msg = (lib().km_last_error() or b"").decode(errors="replace")
+    if rc == KM_EINVAL:
+        raise ConfigurationError(msg)
+    raise DeviceError(msg)

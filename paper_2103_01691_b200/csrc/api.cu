@@ -1,0 +1,277 @@
+// libkmb200 C ABI (include/kmb200.h): argument checks, dtype dispatch, the
+// standalone pointwise pass and the Tucker/step driver.  Kernels live in
+// kmb200_kernels.cuh; each dtype combination is instantiated in inst_*.cu.
+#include "kmb200_launch.cuh"
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+namespace kmb {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(KM_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return KM_OK;
+}
+
+OpDev to_dev(const km_pointop* op) {
+  OpDev o;
+  memset(&o, 0, sizeof(o));
+  if (!op) return o;
+  o.kind = op->kind;
+  o.d = op->d;
+  for (int i = 0; i < KM_MAX_D; ++i) {
+    o.dims[i] = op->dims[i];
+    o.w[i] = op->weights[i];
+  }
+  o.coef = op->coef;
+  o.diag = static_cast<const double2*>(op->diag);
+  o.diag_dir = op->diag_dir;
+  int64_t s = 1;
+  for (int i = 0; i < op->diag_dir && i < op->d; ++i) s *= op->dims[i];
+  o.diag_stride = s;
+  return o;
+}
+
+int validate_op(const km_pointop* op, const char* where) {
+  if (!op || op->kind == KM_OP_NONE) return KM_OK;
+  if (op->d < 1 || op->d > KM_MAX_D) return fail(KM_EINVAL, "%s: op order %d outside 1..%d", where, op->d, KM_MAX_D);
+  if (op->kind == KM_OP_GPE_PHASE) {
+    for (int i = 0; i < op->d; ++i)
+      if (!op->weights[i]) return fail(KM_EINVAL, "%s: GPE phase weight %d is NULL", where, i);
+    return KM_OK;
+  }
+  if (op->kind == KM_OP_DIAG) {
+    if (!op->diag) return fail(KM_EINVAL, "%s: diagonal factor is NULL", where);
+    if (op->diag_dir < 0 || op->diag_dir >= op->d)
+      return fail(KM_EINVAL, "%s: diagonal direction %d outside 0..%d", where, op->diag_dir, op->d - 1);
+    return KM_OK;
+  }
+  return fail(KM_EINVAL, "%s: unknown pointwise op kind %d", where, op->kind);
+}
+
+bool is_complex(int dt) { return dt == KM_C64 || dt == KM_C128; }
+bool is_double(int dt) { return dt == KM_F64 || dt == KM_C128; }
+size_t elem_bytes(int dt) { return dt == KM_F32 ? 4 : (dt == KM_C128 ? 16 : 8); }
+int promote(int a, int b) {
+  const bool c = is_complex(a) || is_complex(b);
+  const bool d = is_double(a) || is_double(b);
+  return c ? (d ? KM_C128 : KM_C64) : (d ? KM_F64 : KM_F32);
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+int pointwise_impl(const void* in, void* out, int dt, int64_t n, const km_pointop* op, cudaStream_t st);
+
+int mumode_impl(const void* u, int udt, const void* L, int ldt, void* out, int64_t m, int64_t nl, int64_t nmu,
+                int64_t nr, const km_pointop* post, cudaStream_t st) {
+  if (udt < KM_F32 || udt > KM_C128 || ldt < KM_F32 || ldt > KM_C128)
+    return fail(KM_EINVAL, "km_mumode: unknown dtype (u=%d, L=%d)", udt, ldt);
+  if (is_double(udt) != is_double(ldt))
+    return fail(KM_EINVAL, "km_mumode: operands must share one precision (u=%d, L=%d)", udt, ldt);
+  if (m < 1 || nl < 1 || nmu < 1 || nr < 1)
+    return fail(KM_EINVAL, "km_mumode: extents must be positive (m=%lld, n_left=%lld, n_mu=%lld, n_right=%lld)",
+                (long long)m, (long long)nl, (long long)nmu, (long long)nr);
+  if (m > 0x7fffffffLL || nmu > 0x7fffffffLL) return fail(KM_EINVAL, "km_mumode: matrix too large");
+  if (!u || !L || !out) return fail(KM_EINVAL, "km_mumode: NULL pointer");
+  int rc0 = validate_op(post, "km_mumode");
+  if (rc0) return rc0;
+  if (post && post->kind != KM_OP_NONE && !(is_complex(udt) || is_complex(ldt)))
+    return fail(KM_EINVAL, "km_mumode: pointwise op needs a complex result");
+  const OpDev op = to_dev(post);
+  const int64_t M = nl * nr;
+  const int N = static_cast<int>(m), K = static_cast<int>(nmu);
+  const bool cu = is_complex(udt), cl = is_complex(ldt);
+  auto launcher = is_double(udt) ? (cu ? (cl ? launch_d_cc : launch_d_cr) : (cl ? launch_d_rc : launch_d_rr))
+                                 : (cu ? (cl ? launch_f_cc : launch_f_cr) : (cl ? launch_f_rc : launch_f_rr));
+  int rc = launcher(u, L, out, M, N, K, nl, op, st);
+  if (rc >= 0) return rc;
+  // op not fusable for this layout/dtype: plain product, then the op in place
+  OpDev none;
+  memset(&none, 0, sizeof(none));
+  if ((rc = launcher(u, L, out, M, N, K, nl, none, st))) return rc;
+  return pointwise_impl(out, out, promote(udt, ldt), M * N, post, st);
+}
+
+template <typename T>
+int pointwise_t(const void* in, void* out, int64_t n, const OpDev& op, cudaStream_t st) {
+  const int threads = 256;
+  int64_t blocks = (n + threads - 1) / threads;
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  if (op.kind == KM_OP_GPE_PHASE)
+    pointwise_kernel<T, KM_OP_GPE_PHASE><<<(unsigned)blocks, threads, 0, st>>>(static_cast<const T*>(in),
+                                                                                static_cast<T*>(out), n, op);
+  else
+    pointwise_kernel<T, KM_OP_DIAG><<<(unsigned)blocks, threads, 0, st>>>(static_cast<const T*>(in),
+                                                                           static_cast<T*>(out), n, op);
+  return check_launch("pointwise_kernel");
+}
+
+int pointwise_impl(const void* in, void* out, int dt, int64_t n, const km_pointop* op, cudaStream_t st) {
+  if (!is_complex(dt)) return fail(KM_EINVAL, "km_pointwise: dtype %d is not complex", dt);
+  if (!op || op->kind == KM_OP_NONE) {
+    if (in != out && n > 0) {
+      cudaError_t e = cudaMemcpyAsync(out, in, n * elem_bytes(dt), cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) return fail(KM_ECUDA, "km_pointwise copy: %s", cudaGetErrorString(e));
+    }
+    return KM_OK;
+  }
+  int rc = validate_op(op, "km_pointwise");
+  if (rc) return rc;
+  if (n <= 0) return KM_OK;
+  const OpDev o = to_dev(op);
+  if (dt == KM_C128) return pointwise_t<double2>(in, out, n, o, st);
+  return pointwise_t<float2>(in, out, n, o, st);
+}
+
+int tucker_plan(int udt, int d, const int64_t* dims, const void* const* mats, const int* mdt, const int64_t* rows,
+                size_t* ws_bytes, int* final_dt) {
+  if (d < 1 || d > KM_MAX_D) return fail(KM_EINVAL, "km_tucker: order %d outside 1..%d", d, KM_MAX_D);
+  if (!dims) return fail(KM_EINVAL, "km_tucker: NULL dims");
+  int64_t cur[KM_MAX_D];
+  for (int i = 0; i < d; ++i) {
+    if (dims[i] < 1) return fail(KM_EINVAL, "km_tucker: extent %d is %lld", i, (long long)dims[i]);
+    cur[i] = dims[i];
+  }
+  int dt = udt;
+  size_t ws = 0;
+  for (int mu = 0; mu < d; ++mu) {
+    if (!mats || !mats[mu]) continue;
+    if (!rows || rows[mu] < 1) return fail(KM_EINVAL, "km_tucker: direction %d has no row count", mu + 1);
+    dt = promote(dt, mdt[mu]);
+    cur[mu] = rows[mu];
+    int64_t n = 1;
+    for (int i = 0; i < d; ++i) n *= cur[i];
+    const size_t b = static_cast<size_t>(n) * elem_bytes(dt);
+    if (b > ws) ws = b;
+  }
+  {  // a standalone pre-pass writes an input-sized copy into the workspace
+    int64_t n = 1;
+    for (int i = 0; i < d; ++i) n *= dims[i];
+    const size_t b = static_cast<size_t>(n) * elem_bytes(udt);
+    if (b > ws) ws = b;
+  }
+  *ws_bytes = ws;
+  *final_dt = dt;
+  return KM_OK;
+}
+
+}  // namespace kmb
+
+using namespace kmb;
+
+// ================================================================== C ABI
+extern "C" {
+
+int km_abi_version(void) { return KMB200_ABI_VERSION; }
+
+const char* km_build_info(void) {
+  return "libkmb200 sm_100a: DMMA.8x8x4 mu-mode GEMM (cp.async 3-stage, 128x64 / 64x32 tiles), fused phase epilogue";
+}
+
+const char* km_last_error(void) { return g_err; }
+
+int km_mumode(const void* u, int u_dtype, const void* L, int L_dtype, void* out, int64_t m, int64_t n_left,
+              int64_t n_mu, int64_t n_right, const km_pointop* post, void* stream) {
+  return mumode_impl(u, u_dtype, L, L_dtype, out, m, n_left, n_mu, n_right, post,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int km_tucker_workspace(int u_dtype, int d, const int64_t* dims, const void* const* mats, const int* mat_dtypes,
+                        const int64_t* rows, size_t* bytes) {
+  int fdt = 0;
+  if (!bytes) return fail(KM_EINVAL, "km_tucker_workspace: NULL output");
+  return tucker_plan(u_dtype, d, dims, mats, mat_dtypes, rows, bytes, &fdt);
+}
+
+int km_pointwise(const void* in, void* out, int dtype, int64_t n, const km_pointop* op, void* stream) {
+  return pointwise_impl(in, out, dtype, n, op, static_cast<cudaStream_t>(stream));
+}
+
+int km_tucker(const void* u, int u_dtype, int d, const int64_t* dims, const void* const* mats,
+              const int* mat_dtypes, const int64_t* rows, void* out, void* ws0, void* ws1, const km_pointop* pre,
+              const km_pointop* post, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  size_t ws = 0;
+  int fdt = 0;
+  int rc = tucker_plan(u_dtype, d, dims, mats, mat_dtypes, rows, &ws, &fdt);
+  if (rc) return rc;
+  if ((rc = validate_op(pre, "km_tucker pre"))) return rc;
+  if ((rc = validate_op(post, "km_tucker post"))) return rc;
+  const bool has_pre = pre && pre->kind != KM_OP_NONE;
+  const bool has_post = post && post->kind != KM_OP_NONE;
+  if ((has_pre && !is_complex(u_dtype)) || (has_post && !is_complex(fdt)))
+    return fail(KM_EINVAL, "km_tucker: pointwise ops need complex tensors");
+
+  int active[KM_MAX_D];
+  int na = 0;
+  for (int mu = 0; mu < d; ++mu)
+    if (mats && mats[mu]) active[na++] = mu;
+  int64_t n_in = 1;
+  for (int i = 0; i < d; ++i) n_in *= dims[i];
+
+  const void* src = u;
+  if (na == 0) {
+    if (has_pre) {
+      if ((rc = pointwise_impl(u, out, u_dtype, n_in, pre, st))) return rc;
+    } else if (u != out && n_in > 0) {
+      cudaError_t e = cudaMemcpyAsync(out, u, n_in * elem_bytes(u_dtype), cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) return fail(KM_ECUDA, "km_tucker copy: %s", cudaGetErrorString(e));
+    }
+    if (has_post) return pointwise_impl(out, out, fdt, n_in, post, st);
+    return KM_OK;
+  }
+  if (((na > 1 || has_pre) && !ws0) || (na > 1 && !ws1)) return fail(KM_EINVAL, "km_tucker: NULL workspace");
+  if (has_pre) {
+    void* dst = (na > 1) ? ws1 : ws0;
+    if ((rc = pointwise_impl(u, dst, u_dtype, n_in, pre, st))) return rc;
+    src = dst;
+  }
+  int64_t cur[KM_MAX_D];
+  for (int i = 0; i < d; ++i) cur[i] = dims[i];
+  int dt = u_dtype;
+  for (int a = 0; a < na; ++a) {
+    const int mu = active[a];
+    int64_t nl = 1, nr = 1;
+    for (int i = 0; i < mu; ++i) nl *= cur[i];
+    for (int i = mu + 1; i < d; ++i) nr *= cur[i];
+    const bool last = (a == na - 1);
+    void* dst = last ? out : (src == ws0 ? ws1 : ws0);
+    if (!last && dst == nullptr) return fail(KM_EINVAL, "km_tucker: NULL workspace");
+    km_pointop post_here;
+    const km_pointop* pp = nullptr;
+    if (last && has_post) {
+      post_here = *post;
+      pp = &post_here;
+    }
+    if ((rc = mumode_impl(src, dt, mats[mu], mat_dtypes[mu], dst, rows[mu], nl, cur[mu], nr, pp, st))) return rc;
+    dt = promote(dt, mat_dtypes[mu]);
+    cur[mu] = rows[mu];
+    src = dst;
+  }
+  return KM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,8 @@
+// Instantiation unit: precision=double, U complex=false, L complex=true.
+#include "kmb200_launch.cuh"
+namespace kmb {
+int launch_d_rc(const void* u, const void* L, void* out, int64_t M, int N, int K, int64_t nl,
+                  const OpDev& op, cudaStream_t st) {
+  return launch_mumode<double, false, true>(u, L, out, M, N, K, nl, op, st);
+}
+}  // namespace kmb

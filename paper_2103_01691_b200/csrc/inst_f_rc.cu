@@ -1,0 +1,8 @@
+// Instantiation unit: precision=float, U complex=false, L complex=true.
+#include "kmb200_launch.cuh"
+namespace kmb {
+int launch_f_rc(const void* u, const void* L, void* out, int64_t M, int N, int K, int64_t nl,
+                  const OpDev& op, cudaStream_t st) {
+  return launch_mumode<float, false, true>(u, L, out, M, N, K, nl, op, st);
+}
+}  // namespace kmb

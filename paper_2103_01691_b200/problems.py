@@ -1,0 +1,247 @@
+"""Splitting and Magnus compositions on the GPU, plus the host setup they need.
+
+Drop-in for the hot-path part of the reference's ``kronmode.problems``:
+
+* :func:`gpe_strang_step` (problems.py:548-565): half nonlinear phase, exact
+  linear step, half nonlinear phase.  One ``km_tucker`` call: the first phase
+  is a standalone pass, the d products run on DMMA and the second phase is
+  fused into the epilogue of the last product; the weight product
+  (problems.py:528-539, rebuilt every step there) is formed in registers from
+  the d weight vectors.
+* :func:`tdpot_strang_step` — the configuration-4 scheme (no reference
+  driver; restated from reference primitives in SURVEY §8(c)): Strang
+  splitting of ``i psi' = H psi + x_3 sin(t)^2 psi`` with the exactly
+  integrated potential phase ``exp(-i x_3 ∫ sin^2)`` fused into the same
+  prologue/epilogue slots.
+* :func:`magnus_midpoint_step` (problems.py:374-382): host exponential of the
+  midpoint generator, device step.
+
+The host helpers (grids, initial states) follow problems.py:273-292,
+496-525.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device as dv
+from . import _native
+from .errors import ConfigurationError, ShapeError
+from .fd import gpe_weighted_factors, sinh_clustered_grid
+from .hermite import position_operator
+from .kron import KroneckerOp, _cache_mats, prepare, step
+from .tensor import _Operand, run_tucker
+
+__all__ = [
+    "VortexProfile",
+    "gpe_setup",
+    "gpe_strang_step",
+    "hkmp_factors",
+    "magnus_midpoint_step",
+    "schrodinger_initial_state",
+    "sin2_integral",
+    "tdpot_phase_factor",
+    "tdpot_strang_step",
+    "ti_potentials",
+    "vortex_pair_state",
+]
+
+
+# ---------------------------------------------------------------------------
+# pointwise operators handed to the C ABI
+
+
+def _gpe_op(shape, weights_dev, half_tau):
+    op = _native.PointOp()
+    op.kind = _native.OP_GPE_PHASE
+    op.d = len(shape)
+    for i, n in enumerate(shape):
+        op.dims[i] = n
+        op.weights[i] = weights_dev[i].data_ptr()
+    op.coef = 0.5 * half_tau  # the i*0.5*half_tau of problems.py:545
+    return op
+
+
+def _diag_op(shape, factor_dev, direction):
+    op = _native.PointOp()
+    op.kind = _native.OP_DIAG
+    op.d = len(shape)
+    for i, n in enumerate(shape):
+        op.dims[i] = n
+    op.diag = factor_dev.data_ptr()
+    op.diag_dir = direction
+    return op
+
+
+def _check_weights(weights, shape):
+    # problems.py:528-539 messages
+    if len(weights) != len(shape):
+        raise ShapeError(f"expected {len(shape)} weight vectors, got {len(weights)}")
+    for ax, w in enumerate(weights):
+        wshape = tuple(w.shape) if dv.is_tensor(w) else np.shape(np.asarray(w, dtype=float))
+        if wshape != (shape[ax],):
+            raise ShapeError(
+                f"direction {ax + 1}: weight vector of shape {wshape} does not match extent {shape[ax]}"
+            )
+
+
+def _strang_dtype(psi_dtype, cache):
+    # the reference's phase multiplies by a complex128 factor (problems.py:545),
+    # so the state leaves the nonlinear half step as complex128 whatever came in
+    return np.result_type(psi_dtype, np.complex128, *(e.dtype for e in cache.exps))
+
+
+def gpe_strang_step(linear_cache, weights, psi, tau, _timer=None):
+    """One Strang step in the weighted variables (problems.py:548-565).
+
+    ``psi <- N(tau/2) ∘ exp(tau*M) ∘ N(tau/2) psi`` with the exact pointwise
+    flow ``N(h) psi = psi * exp(0.5i*h*(1 - |psi|^2/w))``.  ``_timer`` is
+    accepted for signature compatibility; device work is asynchronous, so the
+    whole step is attributed to it.
+    """
+    po = _Operand(psi)
+    if po.shape != linear_cache.shape:
+        raise ShapeError(f"state shape {po.shape} does not match cache shape {linear_cache.shape}")
+    _check_weights(weights, po.shape)
+    if len(po.shape) > _native.MAX_D:
+        raise ConfigurationError(f"the fused Strang step supports at most {_native.MAX_D} directions")
+    out_dtype = _strang_dtype(po.dtype, linear_cache)
+    dev = po.obj.device if po.is_tensor and po.obj.is_cuda else dv.device()
+    w_dev = [dv.cached_vector(w, np.float64, dev) for w in weights]
+    half_tau = 0.5 * tau
+    pre = _gpe_op(po.shape, w_dev, half_tau)
+    post = _gpe_op(po.shape, w_dev, half_tau)
+    state = po.obj
+    if po.dtype != out_dtype and not po.is_tensor:
+        state = np.asarray(state).astype(out_dtype, order="F")
+    elif po.is_tensor and dv.np_dtype(state.dtype) != out_dtype:
+        state = dv.tensor_as(state, out_dtype)
+    mats = _cache_mats(linear_cache, _Operand(state))
+    if _timer is not None:
+        with _timer.mode_products():
+            return run_tucker(state, mats, pre=pre, post=post, out_dtype=out_dtype, keepalive=w_dev)
+    return run_tucker(state, mats, pre=pre, post=post, out_dtype=out_dtype, keepalive=w_dev)
+
+
+def sin2_integral(t_a, t_b):
+    """``∫_{t_a}^{t_b} sin(s)^2 ds = [s/2 - sin(2s)/4]``."""
+    return (t_b / 2 - math.sin(2 * t_b) / 4) - (t_a / 2 - math.sin(2 * t_a) / 4)
+
+
+def tdpot_phase_factor(x, t_a, t_b):
+    """Exact flow of ``i psi' = x sin(t)^2 psi`` over [t_a, t_b]: ``exp(-i x ∫ sin^2)``."""
+    return np.exp(-1j * np.asarray(x, dtype=float) * sin2_integral(t_a, t_b))
+
+
+def tdpot_strang_step(linear_cache, x_nodes, psi, t, tau, direction=3):
+    """One Strang step of ``i psi' = (H_0 + x_dir sin(t)^2) psi`` (configuration 4).
+
+    ``linear_cache`` holds the exact propagators of ``H_0`` for ``tau``
+    (e.g. :func:`hermite.physical_propagator` per direction); the potential
+    flow ``exp(-i x ∫ sin^2)`` over [t, t+tau/2] is applied before and over
+    [t+tau/2, t+tau] after it, both as direction-diagonal factors fused into
+    the product launches.
+    """
+    po = _Operand(psi)
+    if po.shape != linear_cache.shape:
+        raise ShapeError(f"state shape {po.shape} does not match cache shape {linear_cache.shape}")
+    if not 1 <= direction <= len(po.shape):
+        raise ShapeError(f"potential direction {direction} outside 1..{len(po.shape)}")
+    x = np.asarray(x_nodes, dtype=float)
+    if x.shape != (po.shape[direction - 1],):
+        raise ShapeError(f"direction {direction}: node vector of shape {x.shape} does not match extent "
+                         f"{po.shape[direction - 1]}")
+    out_dtype = _strang_dtype(po.dtype, linear_cache)
+    dev = po.obj.device if po.is_tensor and po.obj.is_cuda else dv.device()
+    f_a = dv.cached_vector(tdpot_phase_factor(x, t, t + 0.5 * tau), np.complex128, dev)
+    f_b = dv.cached_vector(tdpot_phase_factor(x, t + 0.5 * tau, t + tau), np.complex128, dev)
+    pre = _diag_op(po.shape, f_a, direction - 1)
+    post = _diag_op(po.shape, f_b, direction - 1)
+    state = po.obj
+    if po.dtype != out_dtype and not po.is_tensor:
+        state = np.asarray(state).astype(out_dtype, order="F")
+    elif po.is_tensor and dv.np_dtype(state.dtype) != out_dtype:
+        state = dv.tensor_as(state, out_dtype)
+    mats = _cache_mats(linear_cache, _Operand(state))
+    return run_tucker(state, mats, pre=pre, post=post, out_dtype=out_dtype, keepalive=(f_a, f_b))
+
+
+def magnus_midpoint_step(factors_of_t, u, t, tau):
+    """Exponential midpoint rule ``u <- exp(tau * M(t + tau/2)) u`` (problems.py:374-382).
+
+    The midpoint exponentials are host scipy ``expm`` (as the reference); the
+    step is the device Tucker product.  Host work for the next call overlaps
+    the device work of this one because device launches are asynchronous.
+    """
+    op = factors_of_t(t + 0.5 * tau)
+    return step(prepare(op, tau), u)
+
+
+def hkmp_factors(basis, t):
+    """Coefficient-space generator of the driven oscillator at time t (problems.py:385-394)."""
+    d_harm = np.diag(np.arange(basis.k) + 0.5)
+    a_static = -1j * d_harm
+    a_driven = -1j * (d_harm + np.sin(t) ** 2 * position_operator(basis))
+    return KroneckerOp((a_static, a_static, a_driven))
+
+
+# ---------------------------------------------------------------------------
+# host setup (problems.py:273-292, 496-525)
+
+
+def schrodinger_initial_state(axes):
+    """``2^(-5/2) π^(-3/4) (x1 + i x2) exp(-(x1²+x2²+x3²)/4)`` on a tensor grid."""
+    x1 = np.asarray(axes[0], dtype=float)[:, None, None]
+    x2 = np.asarray(axes[1], dtype=float)[None, :, None]
+    x3 = np.asarray(axes[2], dtype=float)[None, None, :]
+    env = np.exp(-(x1**2) / 4) * np.exp(-(x2**2) / 4) * np.exp(-(x3**2) / 4)
+    return np.asfortranarray(2.0**-2.5 * np.pi**-0.75 * (x1 + 1j * x2) * env)
+
+
+def ti_potentials():
+    """Per-direction potentials of the time-independent benchmark (problems.py:286-292)."""
+    return (lambda x: np.cos(2 * np.pi * x), lambda x: 0.5 * x * x, lambda x: 0.5 * x * x)
+
+
+@dataclass(frozen=True)
+class VortexProfile:
+    """Rational core profile ``f(r)`` of a straight vortex line (problems.py:477-493)."""
+
+    a1: float = 11.0 / 32.0
+    a2: float = 11.0 / 384.0
+    b1: float = 1.0 / 3.0
+    offset: float = 2.0
+
+    def radial(self, r):
+        r2 = np.asarray(r) ** 2
+        return np.sqrt(r2 * (self.a1 + self.a2 * r2) / (1.0 + self.b1 * r2 + self.a2 * r2**2))
+
+
+def vortex_pair_state(grids, profile=VortexProfile()):
+    """Two orthogonal straight vortices in a unit background (problems.py:496-512)."""
+    x1 = grids[0].points[:, None, None]
+    x2 = grids[1].points[None, :, None]
+    x3 = grids[2].points[None, None, :]
+    dlt = profile.offset
+    psi_a = profile.radial(np.sqrt(x2**2 + (x3 + dlt) ** 2)) * np.exp(1j * np.arctan2(x3 + dlt, x2))
+    psi_b = profile.radial(np.sqrt((x3 - dlt) ** 2 + x1**2)) * np.exp(1j * np.arctan2(x1, x3 - dlt))
+    return np.asfortranarray(psi_a * psi_b)
+
+
+def gpe_setup(n, half_width=20.0, strength=2.0):
+    """Clustered grids, ``i *`` symmetrised half-Laplacian factors, trapezoid weights (problems.py:515-525)."""
+    grids = tuple(sinh_clustered_grid(n, half_width, strength) for _ in range(3))
+    sym_op, weights = gpe_weighted_factors(grids)
+    return grids, KroneckerOp(tuple(1j * a for a in sym_op.factors)), weights
+
+
+def weighted_vortex_state(grids, weights):
+    """``sqrt(w_1 w_2 w_3) * vortex_pair_state`` in F order (problems.py:589-592)."""
+    psi = vortex_pair_state(grids)
+    for ax, w in enumerate(weights):
+        psi = psi * np.sqrt(w).reshape((1,) * ax + (w.size,) + (1,) * (2 - ax))
+    return np.asfortranarray(psi)
+

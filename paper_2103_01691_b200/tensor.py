@@ -1,0 +1,340 @@
+"""Dense order-d tensor kernels on the B200: μ-mode products, Tucker operator, norms.
+
+Drop-in for the reference's ``kronmode.tensor`` (tensor.py:1-199).  Tensors
+are column-major (direction 1 fastest, tensor.py:3-6); directions are
+1-based.  Every product runs on the GPU through ``libkmb200.so``
+(include/kmb200.h ``km_mumode`` / ``km_tucker``) — one DMMA GEMM per product
+over the (n_left, n_mu, n_right) flattening of tensor.py:132-134.
+
+Inputs may be numpy arrays (copied to the device and back: numpy in → numpy
+out, F-ordered, as the reference returns) or CUDA torch tensors with
+column-major strides (kept on the device: tensor in → tensor out).
+Validation, error classes and messages, dtype promotion (``np.result_type``,
+tensor.py:113) and the multiply-add tally (tensor.py:114-115) follow the
+reference so its tests read the same.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from contextlib import contextmanager
+from math import prod
+
+import numpy as np
+
+from . import _device as dv
+from . import _native
+from .errors import ConfigurationError, InvalidDirectionError, ShapeError
+
+__all__ = [
+    "FlopCounter",
+    "count_flops",
+    "mu_fiber_count",
+    "mu_mode_product",
+    "norm",
+    "tucker",
+]
+
+
+class FlopCounter:
+    """Multiply-add tally of the mode products executed while armed (tensor.py:34-40)."""
+
+    __slots__ = ("macs",)
+
+    def __init__(self):
+        self.macs = 0
+
+
+_active_counters: list[FlopCounter] = []
+
+
+@contextmanager
+def count_flops():
+    """Arm a :class:`FlopCounter` for mode products run inside the block (tensor.py:46-59).
+
+    One ``m x n_mu`` product applied to a tensor with ``N/n_mu`` fibers adds
+    ``m * (N/n_mu) * n_mu`` multiply-adds.
+    """
+    counter = FlopCounter()
+    _active_counters.append(counter)
+    try:
+        yield counter
+    finally:
+        _active_counters.remove(counter)
+
+
+def _tally(macs):
+    for counter in _active_counters:
+        counter.macs += macs
+
+
+def _check_direction(ndim, mu):
+    # tensor.py:62-66
+    if not isinstance(mu, (int, np.integer)) or isinstance(mu, bool):
+        raise InvalidDirectionError(f"direction index must be an integer, got {mu!r}")
+    if not 1 <= mu <= ndim:
+        raise InvalidDirectionError(f"direction {mu} outside 1..{ndim}")
+
+
+def mu_fiber_count(shape, mu):
+    """Number of mu-fibers of a tensor with the given extents, ``N / n_mu`` (tensor.py:69-77)."""
+    dims = tuple(int(n) for n in shape)
+    if not dims:
+        raise ShapeError("shape must have at least one extent")
+    if any(n < 1 for n in dims):
+        raise ShapeError(f"extents must be positive, got {dims}")
+    _check_direction(len(dims), mu)
+    return prod(dims) // dims[mu - 1]
+
+
+# --------------------------------------------------------------------------
+# operand handling
+
+
+class _Operand:
+    """A tensor or matrix argument: numpy/torch, its shape and numpy dtype."""
+
+    __slots__ = ("obj", "shape", "dtype", "is_tensor")
+
+    def __init__(self, obj):
+        self.is_tensor = dv.is_tensor(obj)
+        if self.is_tensor:
+            self.obj = obj
+            self.shape = tuple(obj.shape)
+            self.dtype = dv.np_dtype(obj.dtype)
+        else:
+            self.obj = np.asarray(obj)
+            self.shape = self.obj.shape
+            self.dtype = self.obj.dtype
+
+    @property
+    def ndim(self):
+        return len(self.shape)
+
+
+def _compute_dtype(out_dtype):
+    """Device dtype for a numpy result dtype (f16/ints/bools are widened)."""
+    out_dtype = np.dtype(out_dtype)
+    if out_dtype in dv.SUPPORTED:
+        return out_dtype
+    if out_dtype.kind == "c":
+        return np.dtype(np.complex128)
+    if out_dtype == np.float16:
+        return np.dtype(np.float32)
+    if out_dtype.kind in "biuf":
+        return np.dtype(np.float64)
+    raise ConfigurationError(f"unsupported dtype {out_dtype} for a mode product")
+
+
+def _operand_dtype(dtype, single):
+    cplx = np.dtype(dtype).kind == "c"
+    if single:
+        return np.dtype(np.complex64 if cplx else np.float32)
+    return np.dtype(np.complex128 if cplx else np.float64)
+
+
+def _tensor_on_device(op, dtype, dev):
+    if op.is_tensor:
+        t = op.obj
+        if t.device != dev:
+            t = t.to(dev)
+        return dv.tensor_as(t, dtype)
+    return dv.to_device(op.obj, dtype, dev)
+
+
+def run_tucker(u, mats, pre=None, post=None, out_dtype=None, keepalive=()):
+    """Core device driver: ``post(pre(u) x_1 mats[0] ... x_d mats[d-1])``.
+
+    ``u``/``mats`` are already validated.  ``pre``/``post`` are
+    :class:`_native.PointOp` (or None).  ``out_dtype`` forces a result dtype
+    (used by the splitting schemes).  Returns numpy for numpy input and a
+    device tensor for tensor input.
+    """
+    uo = _Operand(u)
+    mos = [None if m is None else _Operand(m) for m in mats]
+    d = uo.ndim
+    result = np.result_type(uo.dtype, *[m.dtype for m in mos if m is not None])
+    if out_dtype is not None:
+        result = np.result_type(result, out_dtype)
+    cdt = _compute_dtype(result)
+    single = cdt in (np.dtype(np.float32), np.dtype(np.complex64))
+    u_dt = _operand_dtype(uo.dtype, single)
+    if (pre is not None or post is not None) and u_dt.kind != "c":
+        u_dt = _operand_dtype(np.complex64, single)
+
+    # the reference's per-product multiply-add tally (tensor.py:114-115)
+    cur = list(uo.shape)
+    for mu, m in enumerate(mos):
+        if m is None:
+            continue
+        _tally(m.shape[0] * prod(cur))
+        cur[mu] = m.shape[0]
+    out_shape = tuple(cur)
+
+    dev = uo.obj.device if uo.is_tensor and uo.obj.is_cuda else dv.device()
+    if any(n == 0 for n in uo.shape) or any(n == 0 for n in out_shape):
+        return _finish(uo, dv.fortran_empty(out_shape, dv.torch_dtype(cdt), dev).zero_(), result, cdt)
+
+    u_dev = _tensor_on_device(uo, u_dt, dev)
+    mats_dev, codes, rows = [], [], []
+    for m in mos:
+        if m is None:
+            mats_dev.append(None)
+            codes.append(0)
+            rows.append(0)
+            continue
+        mdt = _operand_dtype(m.dtype, single)
+        mats_dev.append(dv.cached_vector(m.obj, mdt, dev))
+        codes.append(dv.code(mdt))
+        rows.append(m.shape[0])
+
+    lib = _native.lib()
+    out = dv.fortran_empty(out_shape, dv.torch_dtype(cdt), dev)
+    stream = dv.stream_ptr(dev)
+    if d <= _native.MAX_D:
+        c_dims = (ctypes.c_int64 * d)(*uo.shape)
+        c_mats = (ctypes.c_void_p * d)(*[None if t is None else t.data_ptr() for t in mats_dev])
+        c_codes = (ctypes.c_int * d)(*codes)
+        c_rows = (ctypes.c_int64 * d)(*rows)
+        ws = ctypes.c_size_t(0)
+        u_code = dv.code(u_dt)
+        _native.check(lib.km_tucker_workspace(u_code, d, c_dims, c_mats, c_codes, c_rows, ctypes.byref(ws)))
+        nact = sum(t is not None for t in mats_dev)
+        need = ws.value if (nact > 1 or pre is not None) else 0
+        ws0 = dv.torch.empty(max(need, 1), dtype=dv.torch.uint8, device=dev) if need else None
+        ws1 = dv.torch.empty(max(need, 1), dtype=dv.torch.uint8, device=dev) if need and nact > 1 else None
+        _native.check(
+            lib.km_tucker(
+                u_dev.data_ptr(), u_code, d, c_dims, c_mats, c_codes, c_rows, out.data_ptr(),
+                None if ws0 is None else ws0.data_ptr(), None if ws1 is None else ws1.data_ptr(),
+                None if pre is None else ctypes.byref(pre), None if post is None else ctypes.byref(post),
+                stream,
+            )
+        )
+        del ws0, ws1, keepalive
+    else:
+        if pre is not None or post is not None:
+            raise ConfigurationError(f"pointwise phases support at most {_native.MAX_D} directions")
+        src, src_dt, shape = u_dev, u_dt, list(uo.shape)
+        active = [mu for mu, t in enumerate(mats_dev) if t is not None]
+        if not active:
+            out.copy_(src)
+        for idx, mu in enumerate(active):
+            mdt = _operand_dtype(mos[mu].dtype, single)
+            new_dt = np.result_type(src_dt, mdt)
+            shape_new = list(shape)
+            shape_new[mu] = rows[mu]
+            dst = out if idx == len(active) - 1 else dv.fortran_empty(shape_new, dv.torch_dtype(new_dt), dev)
+            _native.check(
+                lib.km_mumode(
+                    src.data_ptr(), dv.code(src_dt), mats_dev[mu].data_ptr(), codes[mu], dst.data_ptr(),
+                    rows[mu], prod(shape[:mu]), shape[mu], prod(shape[mu + 1:]), None, stream,
+                )
+            )
+            src, src_dt, shape = dst, new_dt, shape_new
+    return _finish(uo, out, result, cdt)
+
+
+def _finish(uo, out, result, cdt):
+    if uo.is_tensor and uo.obj.is_cuda:
+        if result != cdt:
+            out = dv.tensor_as(out, result) if result in dv.SUPPORTED else out.to(dv.torch_dtype(result))
+        return out
+    host = dv.to_host(out)
+    if host.dtype != result:
+        host = host.astype(result, order="F")
+    if uo.is_tensor:  # CPU torch tensor in → CPU torch tensor out
+        return dv.torch.from_numpy(host)
+    return host
+
+
+# --------------------------------------------------------------------------
+# public API
+
+
+def mu_mode_product(u, mat, mu):
+    """Multiply ``mat`` onto every mu-fiber of ``u`` (tensor.py:80-140).
+
+    Returns a column-major tensor of shape ``(n_1, ..., m, ..., n_d)`` with
+    ``S[..., i, ...] = sum_j mat[i, j] * u[..., j, ...]``; real and complex
+    operands mix by numpy promotion.  Computed on the GPU as one DMMA GEMM.
+    """
+    uo = _Operand(u)
+    mo = _Operand(mat)
+    _check_direction(uo.ndim, mu)
+    if mo.ndim != 2:
+        raise ShapeError(f"operator for direction {mu} must be a matrix, got ndim={mo.ndim}")
+    n_mu = uo.shape[mu - 1]
+    if mo.shape[1] != n_mu:
+        raise ShapeError(f"direction {mu}: matrix has {mo.shape[1]} columns, tensor extent is {n_mu}")
+    mats = [None] * uo.ndim
+    mats[mu - 1] = mo.obj
+    return run_tucker(uo.obj, mats)
+
+
+def _validate_tucker(uo, mats):
+    # tensor.py:150-161: every slot is checked before any work
+    if len(mats) != uo.ndim:
+        raise ShapeError(f"expected {uo.ndim} matrix slots, got {len(mats)}")
+    for mu, mat in enumerate(mats, start=1):
+        if mat is None:
+            continue
+        mo = _Operand(mat)
+        if mo.ndim != 2 or mo.shape[1] != uo.shape[mu - 1]:
+            raise ShapeError(
+                f"direction {mu}: matrix of shape {mo.shape} does not act on extent {uo.shape[mu - 1]}"
+            )
+
+
+def tucker(u, mats):
+    """Apply one matrix per direction: ``u x_1 mats[0] x_2 ... x_d mats[d-1]`` (tensor.py:143-166).
+
+    ``None`` entries are skipped; directions are applied in ascending order.
+    """
+    uo = _Operand(u)
+    mats = list(mats)
+    _validate_tucker(uo, mats)
+    if all(m is None for m in mats):
+        return u if uo.is_tensor else uo.obj
+    return run_tucker(uo.obj, mats)
+
+
+def norm(u, kind="two", weights=None):
+    """Tensor norm: ``max``, Euclidean ``two`` or ``weighted_two`` (tensor.py:169-198).
+
+    Reduced on the device (torch reductions; a fused epilogue reduction is the
+    SURVEY §8(f) row 3 follow-up).
+    """
+    uo = _Operand(u)
+    if kind not in ("max", "two", "weighted_two"):
+        raise ConfigurationError(f"unknown norm kind {kind!r}")
+    if kind == "weighted_two":
+        if weights is None:
+            raise ConfigurationError("weighted_two norm requires per-direction weights")
+        if len(weights) != uo.ndim:
+            raise ShapeError(f"expected {uo.ndim} weight vectors, got {len(weights)}")
+        for mu, w in enumerate(weights, start=1):
+            wshape = tuple(np.shape(w)) if not dv.is_tensor(w) else tuple(w.shape)
+            if wshape != (uo.shape[mu - 1],):
+                raise ShapeError(
+                    f"direction {mu}: weight vector of shape {wshape} does not match "
+                    f"extent {uo.shape[mu - 1]}"
+                )
+    if uo.ndim and any(n == 0 for n in uo.shape):
+        if kind == "max":
+            raise ValueError("zero-size array to reduction operation maximum which has no identity")
+        return 0.0
+    dev = uo.obj.device if uo.is_tensor and uo.obj.is_cuda else dv.device()
+    t = _tensor_on_device(uo, _compute_dtype(uo.dtype), dev)
+    a = t.abs()
+    if kind == "max":
+        return float(a.max())
+    if kind == "two":
+        return float(dv.torch.linalg.vector_norm(t.reshape(-1) if t.is_contiguous() else t.flatten()))
+    acc = a * a
+    for mu, w in enumerate(weights):
+        wt = dv.cached_vector(w, np.float64, dev).to(acc.dtype)
+        shape = [1] * uo.ndim
+        shape[mu] = uo.shape[mu]
+        acc = acc * wt.reshape(shape)
+    return float(dv.torch.sqrt(acc.sum()))

@@ -1,0 +1,372 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the CPU oracle on the same seeded inputs.
+
+Bars (north star): relative l2 <= 1e-12 for complex128/float64 and <= 1e-5
+for complex64/float32; bitwise where the reference's own tests are bitwise
+(identity, tau = 0).  Full-size (256^3) cases are checked against the oracle
+directly and through size-independent properties (unitarity, plane-wave
+eigenvectors, direction-order invariance).
+"""
+
+import numpy as np
+import pytest
+
+import paper_2103_01691_b200 as km
+from conftest import golden
+from oracle import kronmode_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+TOL = {np.dtype(np.complex128): 1e-12, np.dtype(np.float64): 1e-12,
+       np.dtype(np.complex64): 1e-5, np.dtype(np.float32): 1e-5}
+
+
+def rel(a, b):
+    return orc.rel_l2(a, b)
+
+
+def crand(rng, shape, dtype=np.complex128):
+    return np.asfortranarray((rng.standard_normal(shape) + 1j * rng.standard_normal(shape)).astype(dtype))
+
+
+def schrod_cache(n, tau=0.01):
+    d2 = km.heat_factors(n, 2).factors[0]
+    return km.prepare(km.KroneckerOp((1j * d2,) * 3), tau)
+
+
+# ------------------------------------------------------------ golden vectors
+
+MUMODE_CASES = sorted({k.split("__")[0] for k in golden("mumode") if not k.startswith("tucker")})
+
+
+@pytest.mark.parametrize("case", MUMODE_CASES)
+def test_mu_mode_product_matches_reference_golden(case):
+    g = golden("mumode")
+    want = g[f"{case}__out"]
+    got = km.mu_mode_product(g[f"{case}__u"], g[f"{case}__mat"], int(g[f"{case}__mu"]))
+    assert got.dtype == want.dtype and got.shape == want.shape
+    assert got.flags.f_contiguous
+    assert rel(got, want) <= TOL[want.dtype]
+
+
+def test_tucker_none_slot_golden():
+    g = golden("mumode")
+    got = km.tucker(g["tucker_none__u"], [g["tucker_none__m0"], None, g["tucker_none__m2"]])
+    assert rel(got, g["tucker_none__out"]) <= 1e-12
+
+
+def test_step_golden_one_and_ten_steps():
+    g = golden("step")
+    cache = km.PropagatorCache(0.01, tuple(g[f"schrod16__e{i}"] for i in range(3)))
+    assert rel(km.step(cache, g["schrod16__u"]), g["schrod16__out"]) <= 1e-12
+    v = g["schrod16__u"]
+    for _ in range(10):
+        v = km.step(cache, v)
+    assert rel(v, g["schrod16__out10"]) <= 1e-12
+    heat = km.PropagatorCache(0.1, (g["heat16__e0"],) * 3)
+    assert rel(km.step(heat, g["heat16__u"]), g["heat16__out"]) <= 1e-12
+
+
+def test_hermite_transforms_golden():
+    g = golden("hermite")
+    b = km.hermite_basis(12)
+    bases = (b,) * 3
+    fwd = km.forward_transform(bases, g["herm12__values"])
+    assert fwd.dtype == g["herm12__forward"].dtype
+    assert rel(fwd, g["herm12__forward"]) <= 1e-12
+    assert rel(km.inverse_transform(bases, g["herm12__forward"]), g["herm12__inverse"]) <= 1e-12
+    pts = [g["herm12__pts0"], g["herm12__pts1"], g["herm12__pts2"]]
+    got = km.inverse_transform(bases, g["herm12__forward"], eval_points=pts)
+    assert got.shape == (7, 5, 2)
+    assert rel(got, g["herm12__inverse_pts"]) <= 1e-12
+
+
+def test_hkp_pipeline_golden():
+    g = golden("hermite")
+    kb = km.hermite_basis(10)
+    c0 = km.forward_transform((kb,) * 3, g["hkp10__psi0"])
+    assert rel(c0, g["hkp10__c0"]) <= 1e-12
+    cache = km.PropagatorCache(1.0, tuple(g[f"hkp10__e{i}"] for i in range(3)))
+    ct = km.step(cache, c0)
+    assert rel(ct, g["hkp10__ct"]) <= 1e-12
+    assert rel(km.inverse_transform((kb,) * 3, ct), g["hkp10__values"]) <= 1e-12
+
+
+def test_magnus_golden():
+    from paper_2103_01691_b200.problems import hkmp_factors
+
+    g = golden("hermite")
+    basis = km.hermite_basis(8)
+    u = g["hkmp8__c0"]
+    tau = 0.5 / 4
+    for s in range(4):
+        u = km.magnus_midpoint_step(lambda t: hkmp_factors(basis, t), u, s * tau, tau)
+    assert rel(u, g["hkmp8__out"]) <= 1e-12
+
+
+def test_gpe_strang_golden():
+    g = golden("gpe")
+    cache = km.PropagatorCache(0.1, tuple(g[f"gpe16__e{i}"] for i in range(3)))
+    ws = [g[f"gpe16__w{i}"] for i in range(3)]
+    p = km.gpe_strang_step(cache, ws, g["gpe16__psi0"], 0.1)
+    assert p.dtype == np.complex128
+    assert rel(p, g["gpe16__out1"]) <= 1e-12
+    for _ in range(4):
+        p = km.gpe_strang_step(cache, ws, p, 0.1)
+    assert rel(p, g["gpe16__out5"]) <= 1e-12
+    c64 = km.PropagatorCache(0.1, tuple(e.astype(np.complex64) for e in cache.exps))
+    p64 = km.gpe_strang_step(c64, ws, g["gpe16__psi0"].astype(np.complex64), 0.1)
+    assert p64.dtype == g["gpe16c64__out1"].dtype
+    assert rel(p64, g["gpe16c64__out1"]) <= 1e-5
+
+
+# ------------------------------------------------ reference test semantics
+
+def test_identity_is_bitwise_identity():
+    rng = np.random.default_rng(7)
+    for u in (np.asfortranarray(rng.random((3, 4, 2)) + 0.5), crand(rng, (3, 4, 2))):
+        for mu in (1, 2, 3):
+            got = km.mu_mode_product(u, np.eye(u.shape[mu - 1]), mu)
+            assert np.array_equal(got, u)
+
+
+def test_row_permutation_exact():
+    u = np.array([[1.0, 2.0], [3.0, 4.0]])
+    swap = np.array([[0.0, 1.0], [1.0, 0.0]])
+    assert np.array_equal(km.mu_mode_product(u, swap, 1), np.array([[3.0, 4.0], [1.0, 2.0]]))
+
+
+def test_random_small_shapes_vs_oracle():
+    rng = np.random.default_rng(123)
+    for trial in range(60):
+        d = int(rng.integers(1, 5))
+        shape = tuple(int(x) for x in rng.integers(1, 5, size=d))
+        mu = int(rng.integers(1, d + 1))
+        rows = int(rng.integers(1, 5))
+        u = rng.standard_normal(shape)
+        if trial % 2:
+            u = u + 1j * rng.standard_normal(shape)
+        mat = rng.standard_normal((rows, shape[mu - 1]))
+        got = km.mu_mode_product(u, mat, mu)
+        want = orc.mu_mode_product(u, mat, mu)
+        scale = max(np.abs(want).max(), 1.0)
+        assert np.abs(got - want).max() <= 1e-14 * scale
+
+
+def test_single_precision_preserved():
+    rng = np.random.default_rng(5)
+    u = rng.standard_normal((4, 4)).astype(np.float32)
+    mat = rng.standard_normal((4, 4)).astype(np.float32)
+    got = km.mu_mode_product(u, mat, 1)
+    assert got.dtype == np.float32
+    assert rel(got, orc.mu_mode_product(u, mat, 1)) <= 1e-5
+
+
+def test_complex_promotion():
+    rng = np.random.default_rng(3)
+    u = rng.standard_normal((2, 3))
+    mat = rng.standard_normal((3, 3)) + 1j * rng.standard_normal((3, 3))
+    got = km.mu_mode_product(u, mat, 2)
+    assert got.dtype == np.complex128
+    assert np.abs(got - orc.mu_mode_product(u, mat, 2)).max() <= 1e-14
+
+
+def test_flop_counter_exact():
+    rng = np.random.default_rng(12)
+    dims = (3, 4, 5)
+    op = km.KroneckerOp(tuple(rng.standard_normal((m, m)) for m in dims))
+    cache = km.prepare(op, 0.2)
+    with km.count_flops() as fc:
+        km.step(cache, np.asfortranarray(rng.standard_normal(dims)))
+    assert fc.macs == sum(60 * m for m in dims)
+
+
+def test_step_zero_increment_bitwise():
+    rng = np.random.default_rng(6)
+    op = km.KroneckerOp((rng.standard_normal((3, 3)), rng.standard_normal((4, 4))))
+    u = np.asfortranarray(rng.standard_normal((3, 4)))
+    assert np.array_equal(km.step(km.prepare(op, 0.0), u), u)
+
+
+def test_step_matches_dense_exponential():
+    rng = np.random.default_rng(9)
+    for trial in range(8):
+        dims = tuple(int(rng.integers(2, 5)) for _ in range(int(rng.integers(2, 4))))
+        facs = []
+        for m in dims:
+            a = rng.standard_normal((m, m))
+            if trial % 2:
+                a = a + 1j * rng.standard_normal((m, m))
+            facs.append(a)
+        op = km.KroneckerOp(tuple(facs))
+        u = np.asfortranarray(rng.standard_normal(dims))
+        tau = float(rng.uniform(0.1, 1.0))
+        got = km.step(km.prepare(op, tau), u).ravel(order="F")
+        want = km.matexp(tau * km.assemble_full(op)) @ u.ravel(order="F")
+        assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want)
+
+
+def test_matvec_vs_dense():
+    rng = np.random.default_rng(3)
+    op = km.KroneckerOp(tuple(rng.standard_normal((m, m)) + 1j * rng.standard_normal((m, m))
+                              for m in (3, 2, 4)))
+    u = np.asfortranarray(rng.standard_normal((3, 2, 4)))
+    want = km.assemble_full(op) @ u.ravel(order="F")
+    got = km.matvec(op, u).ravel(order="F")
+    assert np.abs(got - want).max() <= 1e-13 * np.abs(want).max()
+
+
+def test_norms_on_device():
+    rng = np.random.default_rng(12)
+    u = rng.standard_normal((3, 4)) + 1j * rng.standard_normal((3, 4))
+    w1, w2 = rng.random(3) + 0.1, rng.random(4) + 0.1
+    want = np.sqrt(sum(w1[i] * w2[j] * abs(u[i, j]) ** 2 for i in range(3) for j in range(4)))
+    assert km.norm(u, "weighted_two", weights=[w1, w2]) == pytest.approx(want, rel=1e-13)
+    assert km.norm(u, "two") == pytest.approx(np.linalg.norm(u), rel=1e-14)
+    assert km.norm(u, "max") == pytest.approx(np.abs(u).max(), rel=1e-15)
+
+
+def test_gpe_tau_zero_identity_bitwise_and_modulus():
+    rng = np.random.default_rng(2)
+    _, lin_op, weights = km.gpe_setup(16)
+    psi = crand(rng, (16, 16, 16))
+    got = km.gpe_strang_step(km.prepare(lin_op, 0.0), weights, psi, 0.0)
+    assert np.array_equal(got, psi)
+    stepped = km.gpe_strang_step(km.prepare(lin_op, 0.0), weights, psi, 0.3)
+    assert np.abs(np.abs(stepped) - np.abs(psi)).max() <= 1e-14
+
+
+def test_gpe_unit_background_stationary():
+    n = 32
+    _, lin_op, weights = km.gpe_setup(n)
+    psi = np.ones((n, n, n), dtype=complex, order="F")
+    for ax, w in enumerate(weights):
+        psi = psi * np.sqrt(w).reshape((1,) * ax + (n,) + (1,) * (2 - ax))
+    start = np.asfortranarray(psi)
+    cache = km.prepare(lin_op, 0.1)
+    p = start
+    for _ in range(10):
+        p = km.gpe_strang_step(cache, weights, p, 0.1)
+    assert np.abs(p - start).max() <= 1e-12 * np.abs(start).max()
+
+
+# ------------------------------------------------ config-scale parity
+
+def test_config1_schrodinger_64_ten_steps_vs_oracle():
+    n = 64
+    rng = np.random.default_rng(0)
+    u = crand(rng, (n,) * 3)
+    cache = schrod_cache(n)
+    got, want = u, u
+    for _ in range(10):
+        got = km.step(cache, got)
+        want = orc.step(cache.exps, want)
+    assert rel(got, want) <= 1e-12
+
+
+def test_config2_pipeflow_1024_vs_oracle():
+    n = 1024
+    op = km.pipeflow_factors(n)
+    cache = km.prepare(op, 4.0 / 8)
+    rho, z = np.linspace(0.1, 5.0, n), np.linspace(0.0, 8.0, n)
+    c0 = np.asfortranarray(np.exp(-8.0 * (rho - 2.55) ** 2)[:, None] * np.exp(-8.0 * (z - 1.5) ** 2)[None, :])
+    got = km.step(cache, c0)
+    assert got.dtype == np.float64
+    assert rel(got, orc.step(cache.exps, c0)) <= 1e-12
+    c0c = np.asfortranarray(c0 * (1 + 1j))
+    assert rel(km.step(cache, c0c), orc.step(cache.exps, c0c)) <= 1e-12
+
+
+def test_complex64_step_vs_oracle():
+    n = 64
+    rng = np.random.default_rng(1)
+    u = crand(rng, (n,) * 3, np.complex64)
+    cache = schrod_cache(n)
+    c64 = km.PropagatorCache(0.01, tuple(e.astype(np.complex64) for e in cache.exps))
+    got = km.step(c64, u)
+    assert got.dtype == np.complex64
+    assert rel(got, orc.step(c64.exps, u)) <= 1e-5
+
+
+@pytest.mark.slow
+def test_headline_256_step_vs_oracle_and_properties():
+    n = 256
+    rng = np.random.default_rng(0)
+    u = crand(rng, (n,) * 3)
+    cache = schrod_cache(n)
+    got = km.step(cache, u)
+    assert rel(got, orc.step(cache.exps, u)) <= 1e-12
+    # E_mu is unitary (exp of i * symmetric): the step preserves the 2-norm
+    assert abs(np.linalg.norm(got.ravel()) / np.linalg.norm(u.ravel()) - 1) <= 1e-12
+    # direction order is immaterial (kron.py:115-116)
+    rev = u
+    for mu in (3, 2, 1):
+        rev = km.mu_mode_product(rev, cache.exps[mu - 1], mu)
+    assert rel(rev, got) <= 1e-12
+
+
+@pytest.mark.slow
+def test_headline_256_plane_wave_eigenvector():
+    n, steps, tau = 256, 3, 0.01
+    h = 2 * np.pi / n
+    x = h * np.arange(n)
+    ks = (1, 2, 3)
+    u = np.exp(1j * ks[0] * x)[:, None, None] * np.exp(1j * ks[1] * x)[None, :, None] \
+        * np.exp(1j * ks[2] * x)[None, None, :]
+    u = np.asfortranarray(u)
+    lam = sum((2 * np.cos(k * h) - 2) / h**2 for k in ks)
+    cache = schrod_cache(n, tau)
+    v = u
+    for _ in range(steps):
+        v = km.step(cache, v)
+    assert rel(v, np.exp(1j * tau * steps * lam) * u) <= 1e-12
+
+
+def test_tdpot_strang_vs_oracle():
+    from paper_2103_01691_b200.hermite import physical_propagator
+    from paper_2103_01691_b200.problems import schrodinger_initial_state
+
+    k = 32
+    b = km.hermite_basis(k)
+    tau = 0.02
+    p = physical_propagator(b, tau)
+    cache = km.PropagatorCache(tau, (p, p, p))
+    psi = schrodinger_initial_state((b.nodes,) * 3)
+    got, want = psi, psi
+    for s in range(3):
+        got = km.tdpot_strang_step(cache, b.nodes, got, s * tau, tau)
+        want = orc.tdpot_strang_step(cache.exps, b.nodes, want, s * tau, tau)
+    assert rel(got, want) <= 1e-12
+
+
+def test_physical_propagator_equals_transform_step_transform():
+    from paper_2103_01691_b200.hermite import physical_propagator
+
+    k = 16
+    b = km.hermite_basis(k)
+    rng = np.random.default_rng(4)
+    vals = crand(rng, (k,) * 3)
+    tau = 0.3
+    harm = km.KroneckerOp((-1j * np.diag(np.arange(k) + 0.5),) * 3)
+    via = km.inverse_transform((b,) * 3, km.step(km.prepare(harm, tau), km.forward_transform((b,) * 3, vals)))
+    p = physical_propagator(b, tau)
+    direct = km.step(km.PropagatorCache(tau, (p,) * 3), vals)
+    assert rel(direct, via) <= 1e-12
+
+
+# ------------------------------------------------ device tensors in / out
+
+def test_torch_tensors_stay_on_device():
+    import torch
+
+    from paper_2103_01691_b200 import _device as dv
+
+    n = 32
+    rng = np.random.default_rng(8)
+    u = crand(rng, (n,) * 3)
+    cache = schrod_cache(n)
+    t = dv.to_device(u, np.complex128, torch.device("cuda"))
+    assert dv.is_fortran(t)
+    out = km.step(cache, t)
+    assert isinstance(out, torch.Tensor) and out.is_cuda and dv.is_fortran(out)
+    assert rel(dv.to_host(out), orc.step(cache.exps, u)) <= 1e-12

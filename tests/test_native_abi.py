@@ -1,0 +1,114 @@
+"""CPU: the C-ABI library loads, exports every symbol include/kmb200.h
+declares, and rejects bad arguments before touching the device."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import HAS_CUDA, ROOT
+from paper_2103_01691_b200 import _native
+
+HEADER = os.path.join(ROOT, "include", "kmb200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(km_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_the_binding_exports():
+    assert declared_symbols() == sorted(_native.EXPORTS)
+
+
+def test_library_loads_and_exports_every_symbol():
+    lib = _native.lib()
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    assert lib.km_abi_version() == _native.ABI_VERSION
+    assert b"sm_100a" in lib.km_build_info()
+
+
+def test_library_is_sm100a_cubin():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "-lelf", _native.LIB_PATH], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_struct_layout_matches_header():
+    # km_pointop: 2*int32 + 8*int64 + 8*ptr + double + ptr + 2*int32
+    assert ctypes.sizeof(_native.PointOp) == 8 + 64 + 64 + 8 + 8 + 8
+
+
+def test_bad_dtype_rejected_without_device():
+    lib = _native.lib()
+    rc = lib.km_mumode(None, 7, None, 3, None, 2, 1, 2, 1, None, None)
+    assert rc == _native.KM_EINVAL
+    assert b"dtype" in lib.km_last_error()
+
+
+def test_mixed_precision_rejected():
+    lib = _native.lib()
+    dummy = ctypes.c_void_p(16)
+    rc = lib.km_mumode(dummy, _native.KM_C64, dummy, _native.KM_C128, dummy, 2, 1, 2, 1, None, None)
+    assert rc == _native.KM_EINVAL
+    assert b"precision" in lib.km_last_error()
+
+
+def test_nonpositive_extent_rejected():
+    lib = _native.lib()
+    dummy = ctypes.c_void_p(16)
+    rc = lib.km_mumode(dummy, _native.KM_C128, dummy, _native.KM_C128, dummy, 0, 1, 2, 1, None, None)
+    assert rc == _native.KM_EINVAL
+
+
+def test_bad_op_rejected():
+    lib = _native.lib()
+    dummy = ctypes.c_void_p(16)
+    op = _native.PointOp()
+    op.kind = 9
+    op.d = 3
+    rc = lib.km_mumode(dummy, _native.KM_C128, dummy, _native.KM_C128, dummy, 2, 1, 2, 1,
+                       ctypes.byref(op), None)
+    assert rc == _native.KM_EINVAL and b"unknown pointwise op" in lib.km_last_error()
+    op.kind = _native.OP_GPE_PHASE
+    rc = lib.km_mumode(dummy, _native.KM_C128, dummy, _native.KM_C128, dummy, 2, 1, 2, 1,
+                       ctypes.byref(op), None)
+    assert rc == _native.KM_EINVAL and b"weight" in lib.km_last_error()
+
+
+def test_tucker_workspace_sizes():
+    lib = _native.lib()
+    d = 3
+    dims = (ctypes.c_int64 * d)(16, 8, 4)
+    mats = (ctypes.c_void_p * d)(1, None, 1)
+    codes = (ctypes.c_int * d)(_native.KM_C128, 0, _native.KM_F64)
+    rows = (ctypes.c_int64 * d)(32, 0, 2)
+    nb = ctypes.c_size_t()
+    assert lib.km_tucker_workspace(_native.KM_F64, d, dims, mats, codes, rows, ctypes.byref(nb)) == 0
+    # largest intermediate: after direction 1 → (32, 8, 4) complex128
+    assert nb.value == 32 * 8 * 4 * 16
+
+
+@pytest.mark.skipif(HAS_CUDA, reason="checks the no-GPU failure mode")
+def test_no_cpu_fallback():
+    import paper_2103_01691_b200 as km
+
+    with pytest.raises(km.DeviceError):
+        km.mu_mode_product(np.ones((2, 3)), np.eye(3), 2)
+    with pytest.raises(km.DeviceError):
+        km.step(km.prepare(km.KroneckerOp((np.eye(2),)), 0.1), np.ones(2))
+
+
+def test_missing_library_fails_loudly(monkeypatch):
+    import paper_2103_01691_b200 as km
+
+    monkeypatch.setattr(_native, "_lib", None)
+    monkeypatch.setattr(_native, "LIB_PATH", "/nonexistent/libkmb200.so")
+    with pytest.raises(km.NativeLibraryError):
+        _native.lib()

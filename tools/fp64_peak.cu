@@ -1,0 +1,85 @@
+// FP64 peak microbenchmark for the B200 roofline denominator.
+// Measures (a) mma.sync m8n8k4 f64 (SASS DMMA.8x8x4) and (b) scalar DFMA
+// throughput with register-resident operands, at several warps/SM, timed with
+// CUDA events. Output: one line per variant, TFLOP/s (2 flop per FMA).
+//
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp64_peak fp64_peak.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
+  printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); return 1; } } while (0)
+
+template <int CHAINS>
+__global__ void dmma_loop(double* out, int iters, double seed) {
+  double a = seed + threadIdx.x * 1e-9, b = seed * 0.5;
+  double acc[CHAINS][2];
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) { acc[c][0] = 0.0; acc[c][1] = c * 1e-12; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < CHAINS; ++c) {
+      asm volatile(
+          "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+          : "+d"(acc[c][0]), "+d"(acc[c][1])
+          : "d"(a), "d"(b));
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) s += acc[c][0] + acc[c][1];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+template <int CHAINS>
+__global__ void dfma_loop(double* out, int iters, double seed) {
+  double a = seed + threadIdx.x * 1e-9, b = seed * 0.5;
+  double acc[CHAINS];
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) acc[c] = c * 1e-12;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < CHAINS; ++c) acc[c] = fma(a, b, acc[c]);
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) s += acc[c];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+template <typename K>
+static int run(const char* name, K kern, int warps_per_cta, int ctas_per_sm, int iters, double flop_per_thread_iter) {
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  double* out;
+  CK(cudaMalloc(&out, 4096 * sizeof(double)));
+  dim3 grid(sms * ctas_per_sm), block(32 * warps_per_cta);
+  kern<<<grid, block>>>(out, iters, 1.0);
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0);
+    kern<<<grid, block>>>(out, iters, 1.0);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  double flops = double(grid.x) * block.x * iters * flop_per_thread_iter;
+  printf("%-28s warps/SM=%3d  %.3f ms  %.2f TFLOP/s\n", name, warps_per_cta * ctas_per_sm, best,
+         flops / (best * 1e-3) / 1e12);
+  cudaFree(out);
+  return 0;
+}
+
+int main() {
+  const int iters = 20000;
+  // one m8n8k4 = 256 FMA per warp = 8 FMA per thread = 16 flop per thread.
+  for (int w : {4, 8, 16, 32}) run("dmma m8n8k4 chains=8", dmma_loop<8>, w, 1, iters, 8 * 16.0);
+  run("dmma m8n8k4 chains=16", dmma_loop<16>, 8, 1, iters / 2, 16 * 16.0);
+  run("dmma m8n8k4 chains=2", dmma_loop<2>, 16, 1, iters * 4, 2 * 16.0);
+  for (int w : {8, 16, 32}) run("dfma chains=8", dfma_loop<8>, w, 1, iters * 4, 8 * 2.0);
+  return 0;
+}
