@@ -5,6 +5,7 @@
 //
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp64_peak fp64_peak.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
@@ -74,7 +75,38 @@ static int run(const char* name, K kern, int warps_per_cta, int ctas_per_sm, int
   return 0;
 }
 
-int main() {
+// back-to-back launches for ~seconds: the power-capped sustained rate
+static int sustained(double seconds) {
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  double* out;
+  CK(cudaMalloc(&out, 4096 * sizeof(double)));
+  dim3 grid(sms), block(256);
+  const int iters = 20000;
+  dmma_loop<8><<<grid, block>>>(out, iters, 1.0);
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  // calibrate launches per second
+  cudaEventRecord(e0);
+  for (int i = 0; i < 10; ++i) dmma_loop<8><<<grid, block>>>(out, iters, 1.0);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  int n = (int)(seconds * 1000.0 / (ms / 10));
+  cudaEventRecord(e0);
+  for (int i = 0; i < n; ++i) dmma_loop<8><<<grid, block>>>(out, iters, 1.0);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  cudaEventElapsedTime(&ms, e0, e1);
+  double flops = double(grid.x) * block.x * iters * 8 * 16.0 * n;
+  printf("SUSTAINED dmma m8n8k4 %d launches %.3f s  %.2f TFLOP/s\n", n, ms / 1e3, flops / (ms * 1e-3) / 1e12);
+  cudaFree(out);
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1) return sustained(atof(argv[1]));
   const int iters = 20000;
   // one m8n8k4 = 256 FMA per warp = 8 FMA per thread = 16 flop per thread.
   for (int w : {4, 8, 16, 32}) run("dmma m8n8k4 chains=8", dmma_loop<8>, w, 1, iters, 8 * 16.0);
