@@ -86,6 +86,24 @@ int km_mumode(const void* u, int u_dtype, const void* L, int L_dtype, void* out,
               const km_pointop* post, void* stream);
 
 /*
+ * μ-mode product on blocked ("split") layouts — the fused pack/unpack of the
+ * slab decomposition's all-to-all.  Same as km_mumode (n_left
+ * must be > 1), except that
+ *   - the input's contracted index j is stored in blocks of `in_block`:
+ *     element (l, j, r) is at (j / in_block) * in_block_stride
+ *                              + l + n_left*(j % in_block) + n_left*in_block*r;
+ *   - the output's row index i is stored in blocks of `out_block`:
+ *     element (l, i, r) is at (i / out_block) * out_block_stride
+ *                              + l + n_left*(i % out_block) + n_left*out_block*r.
+ * in_block == n_mu / out_block == m are the plain layouts.  in_block must be a
+ * multiple of 16 and out_block a multiple of 8 when they split.
+ */
+int km_mumode_split(const void* u, int u_dtype, const void* L, int L_dtype, void* out,
+                    int64_t m, int64_t n_left, int64_t n_mu, int64_t n_right,
+                    int32_t in_block, int64_t in_block_stride, int32_t out_block,
+                    int64_t out_block_stride, void* stream);
+
+/*
  * Tucker operator / exact propagator step (reference: tensor.tucker,
  * tensor.py:143-166; kron.step, kron.py:110-121; the Strang composition
  * problems.py:548-565 when pre/post are phases).

@@ -28,6 +28,7 @@ EXPORTS = (
     "km_build_info",
     "km_last_error",
     "km_mumode",
+    "km_mumode_split",
     "km_tucker",
     "km_tucker_workspace",
     "km_pointwise",
@@ -64,6 +65,9 @@ def _declare(lib):
     lib.km_last_error.argtypes = []
     lib.km_mumode.restype = c_int
     lib.km_mumode.argtypes = [c_vp, c_int, c_vp, c_int, c_vp, c_i64, c_i64, c_i64, c_i64, p_op, c_vp]
+    lib.km_mumode_split.restype = c_int
+    lib.km_mumode_split.argtypes = [c_vp, c_int, c_vp, c_int, c_vp, c_i64, c_i64, c_i64, c_i64,
+                                    ctypes.c_int32, c_i64, ctypes.c_int32, c_i64, c_vp]
     lib.km_tucker.restype = c_int
     lib.km_tucker.argtypes = [
         c_vp, c_int, c_int, ctypes.POINTER(c_i64), ctypes.POINTER(c_vp), ctypes.POINTER(c_int),

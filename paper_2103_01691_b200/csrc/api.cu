@@ -84,7 +84,7 @@ int num_sms() {
 int pointwise_impl(const void* in, void* out, int dt, int64_t n, const km_pointop* op, cudaStream_t st);
 
 int mumode_impl(const void* u, int udt, const void* L, int ldt, void* out, int64_t m, int64_t nl, int64_t nmu,
-                int64_t nr, const km_pointop* post, cudaStream_t st) {
+                int64_t nr, const km_pointop* post, cudaStream_t st, const Split* split = nullptr) {
   if (udt < KM_F32 || udt > KM_C128 || ldt < KM_F32 || ldt > KM_C128)
     return fail(KM_EINVAL, "km_mumode: unknown dtype (u=%d, L=%d)", udt, ldt);
   if (is_double(udt) != is_double(ldt))
@@ -101,15 +101,33 @@ int mumode_impl(const void* u, int udt, const void* L, int ldt, void* out, int64
   const OpDev op = to_dev(post);
   const int64_t M = nl * nr;
   const int N = static_cast<int>(m), K = static_cast<int>(nmu);
+  Split sp{K, 0, N, 0};
+  if (split) {
+    const bool ksplit = split->kcb != K, nsplit = split->ncb != N;
+    if (split->kcb < 1 || split->kcb > K || split->ncb < 1 || split->ncb > N)
+      return fail(KM_EINVAL, "km_mumode_split: block sizes (%d, %d) outside (1..%d, 1..%d)", split->kcb,
+                  split->ncb, K, N);
+    if ((ksplit || nsplit) && nl == 1)
+      return fail(KM_EINVAL, "km_mumode_split: blocked layouts need n_left > 1");
+    if (ksplit && split->kcb % BK != 0)
+      return fail(KM_EINVAL, "km_mumode_split: input block %d is not a multiple of %d", split->kcb, BK);
+    if (nsplit && split->ncb % 8 != 0)
+      return fail(KM_EINVAL, "km_mumode_split: output block %d is not a multiple of 8", split->ncb);
+    if ((ksplit || nsplit) && op.kind != KM_OP_NONE)
+      return fail(KM_EINVAL, "km_mumode_split: pointwise ops are not supported on blocked layouts");
+    sp = *split;
+    if (!ksplit) sp.kbs = 0;
+    if (!nsplit) sp.nbs = 0;
+  }
   const bool cu = is_complex(udt), cl = is_complex(ldt);
   auto launcher = is_double(udt) ? (cu ? (cl ? launch_d_cc : launch_d_cr) : (cl ? launch_d_rc : launch_d_rr))
                                  : (cu ? (cl ? launch_f_cc : launch_f_cr) : (cl ? launch_f_rc : launch_f_rr));
-  int rc = launcher(u, L, out, M, N, K, nl, op, st);
+  int rc = launcher(u, L, out, M, N, K, nl, op, sp, st);
   if (rc >= 0) return rc;
   // op not fusable for this layout/dtype: plain product, then the op in place
   OpDev none;
   memset(&none, 0, sizeof(none));
-  if ((rc = launcher(u, L, out, M, N, K, nl, none, st))) return rc;
+  if ((rc = launcher(u, L, out, M, N, K, nl, none, sp, st))) return rc;
   return pointwise_impl(out, out, promote(udt, ldt), M * N, post, st);
 }
 
@@ -197,6 +215,14 @@ int km_mumode(const void* u, int u_dtype, const void* L, int L_dtype, void* out,
               int64_t n_mu, int64_t n_right, const km_pointop* post, void* stream) {
   return mumode_impl(u, u_dtype, L, L_dtype, out, m, n_left, n_mu, n_right, post,
                      static_cast<cudaStream_t>(stream));
+}
+
+int km_mumode_split(const void* u, int u_dtype, const void* L, int L_dtype, void* out, int64_t m, int64_t n_left,
+                    int64_t n_mu, int64_t n_right, int32_t in_block, int64_t in_block_stride, int32_t out_block,
+                    int64_t out_block_stride, void* stream) {
+  Split sp{in_block, in_block_stride, out_block, out_block_stride};
+  return mumode_impl(u, u_dtype, L, L_dtype, out, m, n_left, n_mu, n_right, nullptr,
+                     static_cast<cudaStream_t>(stream), &sp);
 }
 
 int km_tucker_workspace(int u_dtype, int d, const int64_t* dims, const void* const* mats, const int* mat_dtypes,

@@ -8,7 +8,7 @@ namespace kmb {
 
 template <typename S, bool CU, bool CL, bool KC, int OPK, int WM_, int WN_>
 int launch_cfg(const void* u, const void* L, void* out, int64_t M, int N, int K, int64_t nl, const OpDev& op,
-               cudaStream_t st) {
+               const Split& sp, cudaStream_t st) {
   using TU = typename El<S, CU>::T;
   using TL = typename El<S, CL>::T;
   using TO = typename El<S, CU || CL>::T;
@@ -24,7 +24,7 @@ int launch_cfg(const void* u, const void* L, void* out, int64_t M, int N, int K,
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   if (tiles > 0x7fffffffLL) return fail(KM_EINVAL, "km_mumode: %lld tiles exceed the grid limit", (long long)tiles);
   kern<<<static_cast<unsigned>(tiles), 32 * WM_ * WN_, Lay::TOTAL, st>>>(
-      static_cast<const TU*>(u), static_cast<const TL*>(L), static_cast<TO*>(out), M, N, K, nl, op);
+      static_cast<const TU*>(u), static_cast<const TL*>(L), static_cast<TO*>(out), M, N, K, nl, op, sp);
   return check_launch("mumode_kernel");
 }
 
@@ -32,29 +32,29 @@ int launch_cfg(const void* u, const void* L, void* out, int64_t M, int N, int K,
 // 64x32 tiles (2 warps) so that small tensors still spread over all SMs.
 template <typename S, bool CU, bool CL, bool KC, int OPK>
 int launch_sized(const void* u, const void* L, void* out, int64_t M, int N, int K, int64_t nl, const OpDev& op,
-                 cudaStream_t st) {
+                 const Split& sp, cudaStream_t st) {
   const int64_t big = ((M + 127) / 128) * ((N + 63) / 64);
-  if (big >= 2 * num_sms()) return launch_cfg<S, CU, CL, KC, OPK, 4, 2>(u, L, out, M, N, K, nl, op, st);
-  return launch_cfg<S, CU, CL, KC, OPK, 2, 1>(u, L, out, M, N, K, nl, op, st);
+  if (big >= 2 * num_sms()) return launch_cfg<S, CU, CL, KC, OPK, 4, 2>(u, L, out, M, N, K, nl, op, sp, st);
+  return launch_cfg<S, CU, CL, KC, OPK, 2, 1>(u, L, out, M, N, K, nl, op, sp, st);
 }
 
 // Returns KM_OK, or a negative value when the fused op is not instantiated for
 // this combination (the caller then runs the op as a separate pass).
 template <typename S, bool CU, bool CL>
 int launch_mumode(const void* u, const void* L, void* out, int64_t M, int N, int K, int64_t nl, const OpDev& op,
-                  cudaStream_t st) {
+                  const Split& sp, cudaStream_t st) {
   const bool kc = (nl == 1);
   if (op.kind == KM_OP_NONE) {
-    if (kc) return launch_sized<S, CU, CL, true, KM_OP_NONE>(u, L, out, M, N, K, nl, op, st);
-    return launch_sized<S, CU, CL, false, KM_OP_NONE>(u, L, out, M, N, K, nl, op, st);
+    if (kc) return launch_sized<S, CU, CL, true, KM_OP_NONE>(u, L, out, M, N, K, nl, op, sp, st);
+    return launch_sized<S, CU, CL, false, KM_OP_NONE>(u, L, out, M, N, K, nl, op, sp, st);
   }
   // fused phase epilogues: complex x complex products in the strided layout
   // (the last direction of a d >= 2 step, where the splitting schemes need them)
   if constexpr (CU && CL) {
     if (!kc) {
       if (op.kind == KM_OP_GPE_PHASE)
-        return launch_sized<S, CU, CL, false, KM_OP_GPE_PHASE>(u, L, out, M, N, K, nl, op, st);
-      if (op.kind == KM_OP_DIAG) return launch_sized<S, CU, CL, false, KM_OP_DIAG>(u, L, out, M, N, K, nl, op, st);
+        return launch_sized<S, CU, CL, false, KM_OP_GPE_PHASE>(u, L, out, M, N, K, nl, op, sp, st);
+      if (op.kind == KM_OP_DIAG) return launch_sized<S, CU, CL, false, KM_OP_DIAG>(u, L, out, M, N, K, nl, op, sp, st);
     }
   }
   return -1;
@@ -62,7 +62,7 @@ int launch_mumode(const void* u, const void* L, void* out, int64_t M, int N, int
 
 #define KMB_DECLARE_LAUNCHER(NAME)                                                                           \
   int NAME(const void* u, const void* L, void* out, int64_t M, int N, int K, int64_t nl, const OpDev& op, \
-           cudaStream_t st);
+           const Split& sp, cudaStream_t st);
 KMB_DECLARE_LAUNCHER(launch_d_cc)
 KMB_DECLARE_LAUNCHER(launch_d_cr)
 KMB_DECLARE_LAUNCHER(launch_d_rc)

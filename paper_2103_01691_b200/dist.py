@@ -74,17 +74,190 @@ class LocalStepper:
         return out
 
 
-class SlabStepper:
-    """Exact steps of a 3D state split into slabs across the ranks of a process group.
+class SlabPlan:
+    """Index bookkeeping of the slab decomposition of a 3D state over P ranks.
 
-    Placeholder until the fused all-to-all path lands; see DESIGN.md §Multi-GPU.
+    Layout "A": rank r holds ``u[:, :, r*c3:(r+1)*c3]`` as a column-major
+    (n1, n2, c3) array (c3 = n3/P).  Layout "B": rank r holds
+    ``u[:, r*c2:(r+1)*c2, :]`` as (n1, c2, n3) (c2 = n2/P).  Both are
+    contiguous slices of the global column-major array's index space along
+    one direction, so scatter/gather need no reordering of elements inside a
+    slab.  The all-to-all moves blocks of n1*c2*c3 elements:
+
+    * A -> B: rank r sends to rank s the (n1, c2, c3) block with i2 in s's
+      chunk.  The direction-2 product writes its output directly in that
+      per-peer block order (``out_block = c2``), so the send buffer needs no
+      pack pass; the receive buffer, blocks ordered by source rank = i3 chunk,
+      IS the layout-B slab.
+    * B -> A: the send buffer is the layout-B slab itself (the block for peer
+      s is the contiguous i3-chunk of s); the receive buffer holds blocks
+      ordered by source rank = i2 chunk, which the next direction-2 product
+      reads in place (``in_block = c2``), so no unpack pass either.
     """
 
-    launches_per_step = 3
+    def __init__(self, dims, nranks):
+        if len(dims) != 3:
+            raise ValueError("the slab decomposition is implemented for 3D states")
+        n1, n2, n3 = (int(x) for x in dims)
+        if n2 % nranks or n3 % nranks:
+            raise ValueError(f"extents {dims} do not split evenly over {nranks} ranks")
+        self.dims = (n1, n2, n3)
+        self.P = nranks
+        self.c2, self.c3 = n2 // nranks, n3 // nranks
+        self.shape_a = (n1, n2, self.c3)
+        self.shape_b = (n1, self.c2, n3)
+        self.block = n1 * self.c2 * self.c3
+        self.local = n1 * n2 * self.c3
+
+    def slab_a(self, u, rank):
+        return u[:, :, rank * self.c3:(rank + 1) * self.c3]
+
+    def slab_b(self, u, rank):
+        return u[:, rank * self.c2:(rank + 1) * self.c2, :]
+
+    # product calls: (direction index, m, n_left, n_mu, n_right, in_block, in_stride, out_block, out_stride)
+    def even_calls(self):
+        """Layout A: directions 1, 2 (packed output) | exchange | direction 3 in layout B."""
+        n1, n2, n3 = self.dims
+        c2, c3, bs = self.c2, self.c3, self.block
+        before = [(0, n1, 1, n1, n2 * c3, n1, 0, n1, 0),
+                  (1, n2, n1, n2, c3, n2, 0, c2, bs)]
+        after = [(2, n3, n1 * c2, n3, 1, n3, 0, n3, 0)]
+        return before, after
+
+    def odd_calls(self):
+        """Layout B: directions 3, 1 | exchange | direction 2 reading blocked input, into layout A."""
+        n1, n2, n3 = self.dims
+        c2, c3, bs = self.c2, self.c3, self.block
+        before = [(2, n3, n1 * c2, n3, 1, n3, 0, n3, 0),
+                  (0, n1, 1, n1, c2 * n3, n1, 0, n1, 0)]
+        after = [(1, n2, n1, n2, c3, c2, bs, n2, 0)]
+        return before, after
+
+
+class SlabStepper:
+    """Exact steps of a 3D state split into slabs over the ranks of a process group.
+
+    One process per GPU; ``comm`` moves the per-peer blocks (NCCL
+    ``all_to_all_single`` over NVLink, see :class:`NcclExchange`).  Because
+    the factors commute, consecutive steps alternate the direction order
+    ({1,2} | a2a | {3}, then {3,1} | a2a | {2}) so that every step needs ONE
+    exchange; the pack/unpack are fused into the direction-2 product (see
+    :class:`SlabPlan`).  After an odd number of steps the state is in layout
+    B, after an even number in layout A (``self.layout``).
+    """
+
+    def __init__(self, plan, rank, local_a, mats, comm):
+        torch = dv.torch
+        self.plan, self.rank, self.comm = plan, rank, comm
+        self.mats = list(mats)
+        n = plan.local
+        self.a = local_a.reshape(-1) if local_a.dim() > 1 else local_a
+        if self.a.numel() != n:
+            raise ValueError("local slab has the wrong size")
+        self.w = torch.empty_like(self.a)
+        self.send = torch.empty_like(self.a)
+        self.recv = torch.empty_like(self.a)
+        self.layout = "A"
+        self.code = dv.code(dv.np_dtype(self.a.dtype))
+        self.mcodes = [dv.code(dv.np_dtype(m.dtype)) for m in self.mats]
+        self.lib = _native.lib()
+        self.launches_per_step = 3
 
     @classmethod
-    def from_global(cls, u_host, cache, dev):  # pragma: no cover - filled in with the NCCL path
-        raise NotImplementedError("multi-GPU slab stepping is not built yet")
+    def from_global(cls, u_host, cache, dev, group=None):
+        import torch.distributed as tdist
+
+        rank, P = tdist.get_rank(group), tdist.get_world_size(group)
+        plan = SlabPlan(u_host.shape, P)
+        local = dv.to_device(np.asfortranarray(plan.slab_a(u_host, rank)), np.complex128, dev)
+        mats = cache.device_exps((np.complex128,) * 3, dev)
+        return cls(plan, rank, dv.as_fortran(local).permute(2, 1, 0).reshape(-1), mats, NcclExchange(group))
+
+    def _run(self, calls, src, dst_final, scratch):
+        stream = dv.stream_ptr(self.a.device)
+        cur = src
+        for idx, (mu, m, nl, nmu, nr, kcb, kbs, ncb, nbs) in enumerate(calls):
+            dst = dst_final if idx == len(calls) - 1 else scratch
+            _native.check(self.lib.km_mumode_split(
+                cur.data_ptr(), self.code, self.mats[mu].data_ptr(), self.mcodes[mu], dst.data_ptr(),
+                m, nl, nmu, nr, kcb, kbs, ncb, nbs, stream))
+            cur = dst
+
+    def pre_exchange(self):
+        before, _ = self.plan.even_calls() if self.layout == "A" else self.plan.odd_calls()
+        self._run(before, self.a, self.send, self.w)
+        return self.send
+
+    def post_exchange(self):
+        _, after = self.plan.even_calls() if self.layout == "A" else self.plan.odd_calls()
+        self._run(after, self.recv, self.a, self.w)
+        self.layout = "B" if self.layout == "A" else "A"
+
+    def step(self):
+        self.pre_exchange()
+        self.comm.exchange(self.recv, self.send)
+        self.post_exchange()
+
+    def local_state(self):
+        """The local slab as a column-major (n1, n2, c3) [layout A] or (n1, c2, n3) [layout B] tensor view."""
+        shape = self.plan.shape_a if self.layout == "A" else self.plan.shape_b
+        return self.a.reshape(tuple(reversed(shape))).permute(2, 1, 0)
+
+    def time_launches(self, reps=10):  # pragma: no cover - per-launch timing lives in LocalStepper
+        return None
 
 
-del np
+class NcclExchange:
+    """Equal-split all-to-all of flat complex buffers over a torch.distributed group."""
+
+    def __init__(self, group=None):
+        import torch.distributed as tdist
+
+        self.tdist = tdist
+        self.group = group
+
+    def exchange(self, recv, send):
+        t = dv.torch
+        r = t.view_as_real(recv) if recv.is_complex() else recv
+        s = t.view_as_real(send) if send.is_complex() else send
+        self.tdist.all_to_all_single(r.reshape(-1), s.reshape(-1), group=self.group)
+
+
+class VirtualSlabGroup:
+    """P logical ranks of :class:`SlabStepper` in ONE process on ONE device.
+
+    The exchange is a local block permutation (recv_r[block s] = send_s[block r]),
+    so the split-layout kernels and the step schedule run exactly as on P GPUs
+    while nothing waits on another process (SURVEY §4 "virtual-rank" test).
+    """
+
+    def __init__(self, u_host, cache, dev, P):
+        self.plan = SlabPlan(u_host.shape, P)
+        mats = cache.device_exps((np.complex128,) * 3, dev)
+        self.ranks = []
+        for r in range(P):
+            local = dv.to_device(np.asfortranarray(self.plan.slab_a(u_host, r)), np.complex128, dev)
+            flat = local.permute(2, 1, 0).reshape(-1)
+            self.ranks.append(SlabStepper(self.plan, r, flat, mats, comm=None))
+
+    def step(self):
+        P, bs = self.plan.P, self.plan.block
+        sends = [st.pre_exchange() for st in self.ranks]
+        for r, st in enumerate(self.ranks):
+            for s in range(P):
+                st.recv[s * bs:(s + 1) * bs].copy_(sends[s][r * bs:(r + 1) * bs])
+        for st in self.ranks:
+            st.post_exchange()
+
+    def gather(self):
+        """The global state as a host numpy array (column-major)."""
+        n1, n2, n3 = self.plan.dims
+        out = np.empty((n1, n2, n3), dtype=np.complex128, order="F")
+        for r, st in enumerate(self.ranks):
+            loc = dv.to_host(st.local_state())
+            if st.layout == "A":
+                out[:, :, r * self.plan.c3:(r + 1) * self.plan.c3] = loc
+            else:
+                out[:, r * self.plan.c2:(r + 1) * self.plan.c2, :] = loc
+        return out

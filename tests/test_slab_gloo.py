@@ -1,0 +1,128 @@
+"""CPU, world size 2 (gloo): the multi-GPU slab decomposition's schedule and
+block layouts (paper_2103_01691_b200/dist.py) against the single-process
+oracle.  The products run through the oracle with the kernel's blocked
+(split) addressing emulated in numpy; the exchange is a real
+torch.distributed all_to_all_single over gloo.  The GPU kernels' split
+addressing itself is covered by the virtual-rank test in test_gpu_dist.py."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as tdist
+import torch.multiprocessing as mp
+
+from oracle import kronmode_oracle as orc
+from paper_2103_01691_b200 import dist
+
+
+def gather_in(buf, nl, nmu, nr, kcb, kbs):
+    if kcb == nmu:
+        return buf[: nl * nmu * nr].reshape((nl, nmu, nr), order="F")
+    blocks = [buf[b * kbs: b * kbs + nl * kcb * nr].reshape((nl, kcb, nr), order="F") for b in range(nmu // kcb)]
+    return np.concatenate(blocks, axis=1)
+
+
+def scatter_out(buf, x, ncb, nbs):
+    nl, m, nr = x.shape
+    if ncb == m:
+        buf[: x.size] = x.reshape(-1, order="F")
+        return
+    for b in range(m // ncb):
+        buf[b * nbs: b * nbs + nl * ncb * nr] = x[:, b * ncb:(b + 1) * ncb, :].reshape(-1, order="F")
+
+
+class CpuSlabStepper(dist.SlabStepper):
+    """SlabStepper whose products run on the CPU oracle (test double for the kernels)."""
+
+    def __init__(self, plan, rank, local_a, mats_np, comm):
+        self.plan, self.rank, self.comm = plan, rank, comm
+        self.mats = mats_np
+        self.a = local_a.copy()
+        self.w = np.empty_like(self.a)
+        self.send = torch.zeros(self.a.size, dtype=torch.complex128)
+        self.recv = torch.zeros(self.a.size, dtype=torch.complex128)
+        self.layout = "A"
+
+    def _run(self, calls, src, dst_final, scratch):
+        cur = src.numpy() if isinstance(src, torch.Tensor) else src
+        for idx, (mu, m, nl, nmu, nr, kcb, kbs, ncb, nbs) in enumerate(calls):
+            last = idx == len(calls) - 1
+            dst = dst_final if last else scratch
+            dnp = dst.numpy() if isinstance(dst, torch.Tensor) else dst
+            x = gather_in(cur, nl, nmu, nr, kcb, kbs)
+            y = orc.mu_mode_product(x, self.mats[mu], 2)
+            scatter_out(dnp, y, ncb, nbs)
+            cur = dnp
+
+    def pre_exchange(self):
+        before, _ = self.plan.even_calls() if self.layout == "A" else self.plan.odd_calls()
+        self._run(before, self.a, self.send, self.w)
+        return self.send
+
+    def post_exchange(self):
+        _, after = self.plan.even_calls() if self.layout == "A" else self.plan.odd_calls()
+        self._run(after, self.recv, self.a, self.w)
+        self.layout = "B" if self.layout == "A" else "A"
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, dims, steps, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(3)
+        u = np.asfortranarray(rng.standard_normal(dims) + 1j * rng.standard_normal(dims))
+        mats = [rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)) for n in dims]
+        mats = [m / np.linalg.norm(m, 2) for m in mats]
+        plan = dist.SlabPlan(dims, world)
+        local = np.asfortranarray(plan.slab_a(u, rank)).reshape(-1, order="F")
+        st = CpuSlabStepper(plan, rank, local, mats, dist.NcclExchange())
+        for _ in range(steps):
+            st.step()
+        want = u
+        for _ in range(steps):
+            want = orc.step(mats, want)
+        shape = plan.shape_a if st.layout == "A" else plan.shape_b
+        got = st.a.reshape(shape, order="F")
+        ref = plan.slab_a(want, rank) if st.layout == "A" else plan.slab_b(want, rank)
+        q.put((rank, st.layout, orc.rel_l2(got, ref)))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("steps", [1, 2, 3])
+def test_slab_schedule_world2_matches_oracle(steps):
+    world, dims = 2, (6, 32, 8)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(world))
+    for rank, layout, err in res:
+        assert layout == ("B" if steps % 2 else "A")
+        assert err <= 1e-13, (rank, err)
+
+
+def test_slab_plan_rejects_uneven_split():
+    with pytest.raises(ValueError):
+        dist.SlabPlan((8, 10, 8), 4)
+
+
+def test_slab_plan_blocks_partition_the_slab():
+    plan = dist.SlabPlan((4, 8, 8), 4)
+    assert plan.block * plan.P == plan.local
+    assert plan.shape_a == (4, 8, 2) and plan.shape_b == (4, 2, 8)
