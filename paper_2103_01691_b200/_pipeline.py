@@ -1,0 +1,202 @@
+"""Host-pipelined Tucker operator for numpy (host) inputs.
+
+A drop-in call such as ``step(cache, u_numpy)`` has to move the state to the
+device and the result back: 2 x 268 MB over PCIe at n=256^3 c128, about 3x
+the device compute.  This driver hides the compute under the copies:
+
+* the state is cut into C slabs along the LAST direction d, which are
+  contiguous in the column-major host array;
+* slab c goes host→device on a copy stream while the compute stream runs the
+  products of directions 1..d-1 on slab c-1 (those never mix slabs);
+* the direction-d product is then launched in C row blocks of E_d
+  (a row block of a row-major matrix is contiguous), each producing one
+  contiguous output slab, which goes device→host on a second copy stream
+  while the next block is computed.
+
+Pointwise ops (the splitting phases) see each slab as a tensor of its own:
+their index arithmetic is local, so the direction-d weight/diagonal pointer is
+offset to the slab's first index.  Results are identical to the unpipelined
+``km_tucker`` path (same kernels, same per-element arithmetic).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from math import prod
+
+import numpy as np
+
+from . import _device as dv
+from . import _native
+
+MIN_BYTES = 16 << 20
+_streams = {}
+
+
+def _side_streams(dev):
+    key = str(dev)
+    if key not in _streams:
+        _streams[key] = (dv.torch.cuda.Stream(dev), dv.torch.cuda.Stream(dev))
+    return _streams[key]
+
+
+def _chunks(n, parts):
+    parts = max(1, min(parts, n))
+    base, extra = divmod(n, parts)
+    out, start = [], 0
+    for i in range(parts):
+        size = base + (1 if i < extra else 0)
+        out.append((start, size))
+        start += size
+    return out
+
+
+def eligible(host, d):
+    return 2 <= d <= _native.MAX_D and host.nbytes >= MIN_BYTES
+
+
+def _op_for_slab(op, dims, last, start, size):
+    """Copy of a pointwise op restricted to the slab [start, start+size) of the last direction."""
+    if op is None:
+        return None
+    o = _native.PointOp()
+    ctypes.pointer(o)[0] = op
+    o.d = len(dims)
+    for i, n in enumerate(dims):
+        o.dims[i] = n
+    o.dims[last] = size
+    if op.kind == _native.OP_GPE_PHASE:
+        o.weights[last] = op.weights[last] + 8 * start  # f64 vector
+    elif op.kind == _native.OP_DIAG and op.diag_dir == last:
+        o.diag = op.diag + 16 * start  # c128 vector
+    return o
+
+
+def tucker_host_pipelined(host, u_dt, mats_dev, codes, rows, pre, post, out_shape, cdt, dev, parts=8):
+    """``post(pre(host) x_1 mats[0] ... x_d mats[d-1])`` for a host array; returns a host array.
+
+    ``host`` is column-major of numpy dtype ``u_dt`` (complex when ``pre`` or
+    ``post`` is given); ``mats_dev`` are row-major device matrices (None =
+    skip) with dtype codes ``codes``; ``cdt`` is the result dtype.
+    """
+    torch = dv.torch
+    lib = _native.lib()
+    d = host.ndim
+    dims = tuple(host.shape)
+    last = d - 1
+    compute = torch.cuda.current_stream(dev)
+    s_in, s_out = _side_streams(dev)
+    stream_c = ctypes.c_void_p(compute.cuda_stream)
+    slabs = _chunks(dims[last], parts)
+    max_slab = max(sz for _, sz in slabs)
+    inner = prod(dims[:last])
+    u_dt = np.dtype(u_dt)
+    pre_active = [i for i in range(last) if mats_dev[i] is not None]
+    has_last = mats_dev[last] is not None
+
+    # dtype / shape walk of one slab through directions 1..d-1
+    walk, shape, dt = [], list(dims[:last]) + [max_slab], u_dt
+    for mu in pre_active:
+        dt = np.result_type(dt, _code_dtype(codes[mu]))
+        shape = list(shape)
+        shape[mu] = rows[mu]
+        walk.append((mu, dt, prod(shape)))
+    mid_dt = dt
+    mid_shape = tuple(shape[:last]) + (dims[last],)
+    inner_mid = prod(mid_shape[:last])
+    ws_bytes = max([inner * max_slab * u_dt.itemsize] + [n * t.itemsize for _, t, n in walk])
+    ws = [torch.empty(ws_bytes, dtype=torch.uint8, device=dev) for _ in range(2)]
+
+    def view(buf, n, npdt):
+        return buf[: n * np.dtype(npdt).itemsize].view(dv.torch_dtype(npdt))
+
+    src_all = torch.empty(host.size, dtype=dv.torch_dtype(u_dt), device=dev)
+    direct_mid = has_last and not pre_active and pre is None
+    mid_all = None
+    if has_last:
+        mid_all = src_all if direct_mid else torch.empty(prod(mid_shape), dtype=dv.torch_dtype(mid_dt), device=dev)
+    out_dev = torch.empty(prod(out_shape), dtype=dv.torch_dtype(cdt), device=dev)
+    inner_out = prod(out_shape[:last])
+
+    h_t = torch.from_numpy(host.reshape(-1, order="F"))
+    pinned_in = h_t.is_pinned()
+    host_out = torch.empty(tuple(reversed(out_shape)), dtype=dv.torch_dtype(cdt), pin_memory=True)
+    host_out_flat = host_out.reshape(-1)
+
+    def ship(lo, hi):
+        ev = torch.cuda.Event()
+        ev.record(compute)
+        s_out.wait_event(ev)
+        with torch.cuda.stream(s_out):
+            host_out_flat[lo:hi].copy_(out_dev[lo:hi], non_blocking=True)
+
+    def product(src, sdt, mu, m, shape, dst, op, lptr=None):
+        nl, nr = prod(shape[:mu]), prod(shape[mu + 1:])
+        lp = mats_dev[mu].data_ptr() if lptr is None else lptr
+        _native.check(lib.km_mumode(src.data_ptr(), dv.code(sdt), ctypes.c_void_p(lp), codes[mu], dst.data_ptr(),
+                                    m, nl, shape[mu], nr, None if op is None else ctypes.byref(op), stream_c))
+
+    # ---- phase 1: per input slab: H2D, pre op, directions 1..d-1
+    for (start, size) in slabs:
+        lo, hi = inner * start, inner * (start + size)
+        ev = torch.cuda.Event()
+        with torch.cuda.stream(s_in):
+            src_all[lo:hi].copy_(h_t[lo:hi], non_blocking=pinned_in)
+            ev.record(s_in)
+        compute.wait_event(ev)
+        cur, cdtype = src_all[lo:hi], u_dt
+        shape = list(dims[:last]) + [size]
+        final_here = not has_last
+        if pre is not None:
+            dst = view(ws[0], cur.numel(), cdtype) if (pre_active or has_last) else out_dev[lo:hi]
+            if final_here and not pre_active:
+                dst = out_dev[inner_out * start: inner_out * start + cur.numel()]
+            op = _op_for_slab(pre, shape, last, start, size)
+            _native.check(lib.km_pointwise(cur.data_ptr(), dst.data_ptr(), dv.code(cdtype), cur.numel(),
+                                           ctypes.byref(op), stream_c))
+            cur = dst
+        for idx, (mu, ndt, _) in enumerate(walk):
+            new_shape = list(shape)
+            new_shape[mu] = rows[mu]
+            n_new = prod(new_shape)
+            last_pre = idx == len(walk) - 1
+            if last_pre and has_last:
+                dst = mid_all[inner_mid * start: inner_mid * start + n_new]
+            elif last_pre:
+                dst = out_dev[inner_out * start: inner_out * start + n_new]
+            else:
+                dst = view(ws[(idx + 1) % 2], n_new, ndt)
+            op = _op_for_slab(post, new_shape, last, start, size) if (last_pre and final_here) else None
+            product(cur, cdtype, mu, rows[mu], shape, dst, op)
+            cur, cdtype, shape = dst, ndt, new_shape
+        if has_last and not walk and not direct_mid:
+            mid_all[inner_mid * start: inner_mid * start + cur.numel()].copy_(cur)
+        if final_here:
+            olo = inner_out * start
+            if not walk:
+                if pre is None:
+                    out_dev[olo: olo + cur.numel()].copy_(cur)
+                if post is not None:
+                    seg = out_dev[olo: olo + cur.numel()]
+                    op = _op_for_slab(post, shape, last, start, size)
+                    _native.check(lib.km_pointwise(seg.data_ptr(), seg.data_ptr(), dv.code(cdt), seg.numel(),
+                                                   ctypes.byref(op), stream_c))
+            ship(olo, olo + inner_out * size)
+
+    # ---- phase 2: direction d in row blocks of E_d; each output slab D2H as it completes
+    if has_last:
+        row_bytes = dims[last] * _code_dtype(codes[last]).itemsize
+        for (start, size) in _chunks(rows[last], parts):
+            olo = inner_out * start
+            dst = out_dev[olo: olo + inner_out * size]
+            op = _op_for_slab(post, list(out_shape[:last]) + [size], last, start, size)
+            product(mid_all, mid_dt, last, size, list(mid_shape), dst, op,
+                    lptr=mats_dev[last].data_ptr() + start * row_bytes)
+            ship(olo, olo + inner_out * size)
+    s_out.synchronize()
+    return host_out.permute(*reversed(range(d))).numpy()
+
+
+def _code_dtype(code):
+    return {_native.KM_F32: np.dtype(np.float32), _native.KM_F64: np.dtype(np.float64),
+            _native.KM_C64: np.dtype(np.complex64), _native.KM_C128: np.dtype(np.complex128)}[code]

@@ -24,6 +24,7 @@ import numpy as np
 
 from . import _device as dv
 from . import _native
+from . import _pipeline
 from .errors import ConfigurationError, InvalidDirectionError, ShapeError
 
 __all__ = [
@@ -175,7 +176,6 @@ def run_tucker(u, mats, pre=None, post=None, out_dtype=None, keepalive=()):
     if any(n == 0 for n in uo.shape) or any(n == 0 for n in out_shape):
         return _finish(uo, dv.fortran_empty(out_shape, dv.torch_dtype(cdt), dev).zero_(), result, cdt)
 
-    u_dev = _tensor_on_device(uo, u_dt, dev)
     mats_dev, codes, rows = [], [], []
     for m in mos:
         if m is None:
@@ -188,6 +188,14 @@ def run_tucker(u, mats, pre=None, post=None, out_dtype=None, keepalive=()):
         codes.append(dv.code(mdt))
         rows.append(m.shape[0])
 
+    if not uo.is_tensor and _pipeline.eligible(uo.obj, d):
+        # host in / host out: overlap the PCIe copies with the products
+        host = np.asfortranarray(uo.obj if uo.dtype == u_dt else uo.obj.astype(u_dt, order="F"))
+        res = _pipeline.tucker_host_pipelined(host, u_dt, mats_dev, codes, rows, pre, post, out_shape, cdt, dev)
+        del keepalive
+        return res if res.dtype == result else res.astype(result, order="F")
+
+    u_dev = _tensor_on_device(uo, u_dt, dev)
     lib = _native.lib()
     out = dv.fortran_empty(out_shape, dv.torch_dtype(cdt), dev)
     stream = dv.stream_ptr(dev)
