@@ -281,8 +281,9 @@ def run_ours(args):
         pinned_np[...] = u_host.transpose(2, 1, 0)  # C-order buffer ...
         host_in = pinned_np.transpose(2, 1, 0)      # ... viewed column-major, same memory
         assert host_in.flags.f_contiguous
-        e2e_steps = max(3, min(args.steps, 20))
-        out = km.step(cache, host_in)  # warm-up (pinned-memory path, allocator warm)
+        e2e_steps = max(3, min(args.steps, 30))
+        for _ in range(max(args.warmup, 3)):  # warm-up: device allocator, pinned result pool, module loading
+            out = km.step(cache, host_in)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):

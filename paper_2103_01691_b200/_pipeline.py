@@ -120,8 +120,8 @@ def tucker_host_pipelined(host, u_dt, mats_dev, codes, rows, pre, post, out_shap
 
     h_t = torch.from_numpy(host.reshape(-1, order="F"))
     pinned_in = h_t.is_pinned()
-    host_out = torch.empty(tuple(reversed(out_shape)), dtype=dv.torch_dtype(cdt), pin_memory=True)
-    host_out_flat = host_out.reshape(-1)
+    host_arr = dv.pinned_host_array(out_shape, cdt)
+    host_out_flat = torch.from_numpy(host_arr.reshape(-1, order="F"))
 
     def ship(lo, hi):
         ev = torch.cuda.Event()
@@ -186,7 +186,9 @@ def tucker_host_pipelined(host, u_dt, mats_dev, codes, rows, pre, post, out_shap
     # ---- phase 2: direction d in row blocks of E_d; each output slab D2H as it completes
     if has_last:
         row_bytes = dims[last] * _code_dtype(codes[last]).itemsize
-        for (start, size) in _chunks(rows[last], parts):
+        # row blocks of whole 64-row output tiles, so no launch pays for a padded tile
+        parts2 = max(1, min(parts, rows[last] // 64)) if rows[last] >= 64 else 1
+        for (start, size) in _chunks(rows[last], parts2):
             olo = inner_out * start
             dst = out_dev[olo: olo + inner_out * size]
             op = _op_for_slab(post, list(out_shape[:last]) + [size], last, start, size)
@@ -194,7 +196,7 @@ def tucker_host_pipelined(host, u_dt, mats_dev, codes, rows, pre, post, out_shap
                     lptr=mats_dev[last].data_ptr() + start * row_bytes)
             ship(olo, olo + inner_out * size)
     s_out.synchronize()
-    return host_out.permute(*reversed(range(d))).numpy()
+    return host_arr
 
 
 def _code_dtype(code):
