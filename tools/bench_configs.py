@@ -1,0 +1,218 @@
+"""Measure every BASELINE.json config on one B200 against the CPU reference algorithm.
+
+    python tools/bench_configs.py [--cpu-budget S] [--out profiles/rNN_configs.json]
+
+Each config: device time (CUDA events, device-resident state, warmed up),
+achieved TFLOP/s at the SURVEY §8(d) flop convention, parity against the CPU
+oracle on the same inputs, and the oracle's own time on the host cores
+(bounded sample).  The headline config (256^3 exact step) is bench.py's job.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+from threadpoolctl import threadpool_limits  # noqa: E402
+
+import paper_2103_01691_b200 as km  # noqa: E402
+from oracle import kronmode_oracle as orc  # noqa: E402
+from paper_2103_01691_b200 import _device as dv  # noqa: E402
+from paper_2103_01691_b200 import dist  # noqa: E402
+from paper_2103_01691_b200.hermite import physical_propagator  # noqa: E402
+from paper_2103_01691_b200.problems import schrodinger_initial_state, weighted_vortex_state  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+def dev_time(fn, reps, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(reps):
+        fn()
+    e1.record(s)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def cpu_time(fn, budget, max_reps=5):
+    fn()  # warm-up
+    ts = []
+    t_end = time.perf_counter() + budget
+    while len(ts) < max_reps:
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end:
+            break
+    return min(ts) * 1e3, len(ts)
+
+
+def crand(rng, shape):
+    return np.asfortranarray(rng.standard_normal(shape) + 1j * rng.standard_normal(shape))
+
+
+def schrod(n, tau=0.01):
+    d2 = km.heat_factors(n, 2).factors[0]
+    return km.prepare(km.KroneckerOp((1j * d2,) * 3), tau)
+
+
+def config1(budget):
+    n, steps = 64, 10
+    u = crand(np.random.default_rng(0), (n,) * 3)
+    cache = schrod(n)
+    st = dist.LocalStepper(dv.to_device(u, np.complex128, DEV), cache.device_exps((np.complex128,) * 3, DEV))
+
+    def ten():
+        for _ in range(steps):
+            st.step()
+
+    ms = dev_time(ten, 20)
+    # graph-captured variant: the 30 launches replayed as one graph
+    st2 = dist.LocalStepper(dv.to_device(u, np.complex128, DEV), cache.device_exps((np.complex128,) * 3, DEV))
+    for _ in range(3):
+        st2.step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(steps):
+                st2.step()
+    torch.cuda.synchronize()
+    ms_graph = dev_time(g.replay, 50)
+    got = u
+    for _ in range(steps):
+        got = km.step(cache, got)
+    want = u
+    for _ in range(steps):
+        want = orc.step(cache.exps, want)
+    cpu_ms, k = cpu_time(lambda: [orc.step(cache.exps, u) for _ in range(steps)], budget)
+    flop = 8 * 3 * n**4 * steps
+    return {"config": "1: 3D Schrodinger free 64^3 c128, 10 steps", "gpu_ms": ms, "gpu_ms_graph": ms_graph,
+            "tflops": flop / (min(ms, ms_graph) * 1e-3) / 1e12, "cpu_ms": cpu_ms, "cpu_reps": k,
+            "speedup": cpu_ms / min(ms, ms_graph), "parity_rel_l2": orc.rel_l2(got, want)}
+
+
+def config2(budget):
+    n = 1024
+    op = km.pipeflow_factors(n)
+    cache = km.prepare(op, 4.0 / 8)
+    rho, z = np.linspace(0.1, 5.0, n), np.linspace(0.0, 8.0, n)
+    c0 = np.asfortranarray(np.exp(-8.0 * (rho - 2.55) ** 2)[:, None] * np.exp(-8.0 * (z - 1.5) ** 2)[None, :])
+    st = dist.LocalStepper(dv.to_device(c0, np.float64, DEV), cache.device_exps((np.float64,) * 2, DEV))
+    ms = dev_time(st.step, 50)
+    cpu_ms, k = cpu_time(lambda: orc.step(cache.exps, c0), budget, 20)
+    flop = 2 * 2 * n**3
+    return {"config": "2: 2D pipe flow 1024^2 f64, one exact step", "gpu_ms": ms,
+            "tflops": flop / (ms * 1e-3) / 1e12, "cpu_ms": cpu_ms, "cpu_reps": k, "speedup": cpu_ms / ms,
+            "parity_rel_l2": orc.rel_l2(km.step(cache, c0), orc.step(cache.exps, c0))}
+
+
+def config3(budget, k=256):
+    b = km.hermite_basis(k)
+    bases = (b,) * 3
+    psi0 = schrodinger_initial_state((b.nodes,) * 3)
+    op = km.KroneckerOp(tuple(km.hamiltonian_factor(b, v) for v in
+                              (lambda x: np.cos(2 * np.pi * x), lambda x: 0.5 * x * x, lambda x: 0.5 * x * x)))
+    cache = km.prepare(op, 1.0)
+    p_dev = dv.to_device(psi0, np.complex128, DEV)
+
+    def hkp():
+        c = km.forward_transform(bases, p_dev)
+        c = km.step(cache, c)
+        return km.inverse_transform(bases, c)
+
+    ms = dev_time(hkp, 10)
+    got = dv.to_host(hkp())
+    fwd_o = lambda: orc.forward_transform([b.phi] * 3, [b.mod_weights] * 3, psi0)  # noqa: E731
+
+    def hkp_cpu():
+        c = fwd_o()
+        c = orc.step(cache.exps, c)
+        return orc.inverse_transform([b.phi.T] * 3, c)
+
+    want = hkp_cpu()
+    cpu_ms, kk = cpu_time(hkp_cpu, budget, 3)
+    flop = 4 * 3 * k**4 * 2 + 8 * 3 * k**4
+    return {"config": "3: HKP 256^3 c128 forward + exact step + inverse", "gpu_ms": ms,
+            "tflops": flop / (ms * 1e-3) / 1e12, "cpu_ms": cpu_ms, "cpu_reps": kk, "speedup": cpu_ms / ms,
+            "parity_rel_l2": orc.rel_l2(got, want)}
+
+
+def config4(budget, k=256):
+    b = km.hermite_basis(k)
+    tau = 0.02
+    p = physical_propagator(b, tau)
+    cache = km.PropagatorCache(tau, (p, p, p))
+    psi = schrodinger_initial_state((b.nodes,) * 3)
+    p_dev = dv.to_device(psi, np.complex128, DEV)
+    ms = dev_time(lambda: km.tdpot_strang_step(cache, b.nodes, p_dev, 0.3, tau), 10)
+    got = km.tdpot_strang_step(cache, b.nodes, psi, 0.3, tau)
+    want = orc.tdpot_strang_step(cache.exps, b.nodes, psi, 0.3, tau)
+    cpu_ms, kk = cpu_time(lambda: orc.tdpot_strang_step(cache.exps, b.nodes, psi, 0.3, tau), budget, 3)
+    # 8-rank slab decomposition run as 8 virtual ranks on this one GPU (schedule + fused pack/unpack kernels)
+    grp = dist.VirtualSlabGroup(psi, cache, DEV, 8)
+    ms_virtual8 = dev_time(grp.step, 5, warm=1)
+    flop = 8 * 3 * k**4
+    return {"config": "4: TD-potential Strang 256^3 c128 (1 GPU; 8-rank schedule as virtual ranks)",
+            "gpu_ms": ms, "tflops": flop / (ms * 1e-3) / 1e12, "cpu_ms": cpu_ms, "cpu_reps": kk,
+            "speedup": cpu_ms / ms, "parity_rel_l2": orc.rel_l2(got, want),
+            "virtual8_linear_step_ms": ms_virtual8}
+
+
+def config5(budget, n=512):
+    grids, lin_op, weights = km.gpe_setup(n)
+    psi = weighted_vortex_state(grids, weights)
+    tau = 0.1
+    cache = km.prepare(lin_op, tau)
+    p_dev = dv.to_device(psi, np.complex128, DEV)
+    ms = dev_time(lambda: km.gpe_strang_step(cache, weights, p_dev, tau), 5)
+    got = km.gpe_strang_step(cache, weights, psi, tau)
+    want = orc.gpe_strang_step(cache.exps, weights, psi, tau)
+    cpu_ms, kk = cpu_time(lambda: orc.gpe_strang_step(cache.exps, weights, psi, tau), budget, 1)
+    c64 = km.PropagatorCache(tau, tuple(e.astype(np.complex64) for e in cache.exps))
+    p64 = dv.to_device(psi.astype(np.complex64), np.complex64, DEV)
+    ms64 = dev_time(lambda: km.gpe_strang_step(c64, weights, p64, tau), 5)
+    flop = 8 * 3 * n**4
+    return {"config": "5: GPE 512^3 Strang step c128 (c64 input follows the reference's promotion to c128)",
+            "gpu_ms": ms, "gpu_ms_c64_input": ms64, "tflops": flop / (ms * 1e-3) / 1e12, "cpu_ms": cpu_ms,
+            "cpu_reps": kk, "speedup": cpu_ms / ms, "parity_rel_l2": orc.rel_l2(got, want)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--only", default="12345")
+    args = ap.parse_args()
+    cores = os.cpu_count() or 1
+    res = {"cores": cores, "configs": []}
+    fns = {"1": config1, "2": config2, "3": config3, "4": config4, "5": config5}
+    with threadpool_limits(limits=cores):
+        for key in args.only:
+            t0 = time.time()
+            r = fns[key](args.cpu_budget)
+            r["wall_s"] = time.time() - t0
+            print(json.dumps(r), flush=True)
+            res["configs"].append(r)
+    if args.out:
+        with open(args.out, "w") as f:
+            json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
