@@ -65,6 +65,12 @@ typedef struct km_pointop {
   int32_t pad_;
 } km_pointop;
 
+/* kernel selection (process-wide): AUTO picks the warp-specialised TMA
+ * kernel for complex128 products whose shape allows it; NO_TMA forces the
+ * cp.async kernel everywhere (A/B testing and verification) */
+enum km_kernel_policy { KM_POLICY_AUTO = 0, KM_POLICY_NO_TMA = 1 };
+int km_set_kernel_policy(int policy);
+
 /* ABI version and build info */
 int km_abi_version(void);
 const char* km_build_info(void);

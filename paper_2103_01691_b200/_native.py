@@ -21,6 +21,7 @@ MAX_D = 8
 KM_F32, KM_F64, KM_C64, KM_C128 = 0, 1, 2, 3
 KM_OK, KM_EINVAL, KM_ECUDA = 0, 1, 2
 OP_NONE, OP_GPE_PHASE, OP_DIAG = 0, 1, 2
+POLICY_AUTO, POLICY_NO_TMA = 0, 1
 
 # every symbol include/kmb200.h declares
 EXPORTS = (
@@ -32,6 +33,7 @@ EXPORTS = (
     "km_tucker",
     "km_tucker_workspace",
     "km_pointwise",
+    "km_set_kernel_policy",
 )
 
 
@@ -78,6 +80,8 @@ def _declare(lib):
         c_int, c_int, ctypes.POINTER(c_i64), ctypes.POINTER(c_vp), ctypes.POINTER(c_int),
         ctypes.POINTER(c_i64), ctypes.POINTER(c_sz),
     ]
+    lib.km_set_kernel_policy.restype = c_int
+    lib.km_set_kernel_policy.argtypes = [c_int]
     lib.km_pointwise.restype = c_int
     lib.km_pointwise.argtypes = [c_vp, c_vp, c_int, c_i64, p_op, c_vp]
 

@@ -9,6 +9,7 @@
 
 namespace kmb {
 
+extern bool g_tma_disabled;  // inst_tma_c128.cu
 thread_local char g_err[512] = "";
 
 int fail(int code, const char* fmt, ...) {
@@ -204,6 +205,13 @@ using namespace kmb;
 extern "C" {
 
 int km_abi_version(void) { return KMB200_ABI_VERSION; }
+
+int km_set_kernel_policy(int policy) {
+  if (policy != KM_POLICY_AUTO && policy != KM_POLICY_NO_TMA)
+    return fail(KM_EINVAL, "km_set_kernel_policy: unknown policy %d", policy);
+  g_tma_disabled = (policy == KM_POLICY_NO_TMA);
+  return KM_OK;
+}
 
 const char* km_build_info(void) {
   return "libkmb200 sm_100a: DMMA.8x8x4 mu-mode GEMM (cp.async 3-stage, 128x64 / 64x32 tiles), fused phase epilogue";

@@ -1,0 +1,97 @@
+// Host side of mumode_tma_kernel: eligibility, TMA tensor maps, persistent launch.
+#include "kmb200_tma.cuh"
+
+#include <cudaTypedefs.h>
+
+namespace kmb {
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+              const cuuint32_t* box) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <bool KC, int OPK>
+int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* out, int64_t M, int N, int K, int64_t nl,
+           const OpDev& op, const Split& sp, cudaStream_t st) {
+  auto kern = mumode_tma_kernel<KC, OPK>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tma::SMEM_BYTES);
+    if (e != cudaSuccess) return fail(KM_ECUDA, "cudaFuncSetAttribute(tma): %s", cudaGetErrorString(e));
+    attr = true;
+  }
+  const int64_t tiles = ((M + tma::BM - 1) / tma::BM) * ((N + tma::BN - 1) / tma::BN);
+  const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
+  kern<<<grid, tma::THREADS, tma::SMEM_BYTES, st>>>(ma, mb, static_cast<double2*>(out), M, N, K, nl, op, sp);
+  return check_launch("mumode_tma_kernel");
+}
+
+}  // namespace
+
+bool g_tma_disabled = false;
+
+int launch_tma_c128(const void* u, const void* L, void* out, int64_t M, int N, int K, int64_t nl, const OpDev& op,
+                    const Split& sp, cudaStream_t st) {
+  if (g_tma_disabled) return -1;
+  const bool kc = (nl == 1);
+  const int64_t tiles = ((M + tma::BM - 1) / tma::BM) * ((N + tma::BN - 1) / tma::BN);
+  if (K % 8 != 0 || tiles < 2 * num_sms()) return -1;
+  if ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(L)) & 15) return -1;
+  if (!kc && (nl % tma::BM != 0 || (sp.kcb != K && sp.kcb % tma::BKS != 0))) return -1;
+  if (op.kind != KM_OP_NONE && kc) return -1;  // fused ops only in the strided layout
+  if (static_cast<int64_t>(K) * 16 >= (int64_t(1) << 40) || M >= (int64_t(1) << 32)) return -1;
+
+  CUtensorMap ma, mb;
+  {  // B: row-major factor, dims (16 f64 = 8 complex k, rows, k groups)
+    cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(K / 8)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(K) * 16, 128};
+    cuuint32_t box[3] = {16, tma::BN, 2};
+    if (!make_map(&mb, L, 3, dims, strides, box)) return -1;
+  }
+  if (kc) {
+    cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(K / 8)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(K) * 16, 128};
+    cuuint32_t box[3] = {16, tma::BM, 2};
+    if (!make_map(&ma, u, 3, dims, strides, box)) return -1;
+  } else {
+    const int64_t nr = M / nl;
+    const int64_t nblk = (K + sp.kcb - 1) / sp.kcb;
+    const int64_t kbs = nblk > 1 ? sp.kbs : static_cast<int64_t>(nl) * sp.kcb * nr;
+    cuuint64_t dims[5] = {16, static_cast<cuuint64_t>(sp.kcb), static_cast<cuuint64_t>(nl / 8),
+                          static_cast<cuuint64_t>(nr), static_cast<cuuint64_t>(nblk)};
+    cuuint64_t strides[4] = {static_cast<cuuint64_t>(nl) * 16, 128, static_cast<cuuint64_t>(nl) * sp.kcb * 16,
+                             static_cast<cuuint64_t>(kbs) * 16};
+    cuuint32_t box[5] = {16, tma::BKS, tma::BM / 8, 1, 1};
+    if (!make_map(&ma, u, 5, dims, strides, box)) return -1;
+  }
+  if (kc) return launch<true, KM_OP_NONE>(ma, mb, out, M, N, K, nl, op, sp, st);
+  switch (op.kind) {
+    case KM_OP_GPE_PHASE: return launch<false, KM_OP_GPE_PHASE>(ma, mb, out, M, N, K, nl, op, sp, st);
+    case KM_OP_DIAG: return launch<false, KM_OP_DIAG>(ma, mb, out, M, N, K, nl, op, sp, st);
+    default: return launch<false, KM_OP_NONE>(ma, mb, out, M, N, K, nl, op, sp, st);
+  }
+}
+
+}  // namespace kmb

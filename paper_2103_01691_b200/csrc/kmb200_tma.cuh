@@ -1,0 +1,239 @@
+// mumode_tma_kernel — warp-specialised, persistent complex128 μ-mode GEMM.
+//
+// Same GEMM view and DMMA arithmetic as mumode_kernel (kmb200_kernels.cuh),
+// re-organised for the B200:
+//   * TMA tile loads (cp.async.bulk.tensor, 128-B swizzle) for A (the tensor)
+//     and B (the factor) into a 4-stage shared-memory ring, issued by ONE lane
+//     (warp 0, lane 0) two k-blocks ahead of the compute and signalled on
+//     per-stage "full" mbarriers with the expected byte count;
+//   * all eight warps wait on "full", run their 4x4-tile DMMA.8x8x4 warp tiles
+//     straight out of the swizzled stage, and release the stage with one
+//     arrive per warp on its "empty" mbarrier — no __syncthreads in the loop.
+//     (A dedicated producer warp would put a third warp on one SM
+//     sub-partition and cap every thread at 168 registers; the accumulators
+//     alone need 128.)
+//   * the grid is persistent (one CTA per SM) and walks the tiles with a
+//     static stride; the k-block counter runs across tiles, so the loads of
+//     tile i+1 are in flight during the epilogue of tile i.
+//
+// Shared-memory tiles are the TMA boxes, 128-B rows with the hardware
+// 16-B-chunk XOR swizzle (chunk ^= row % 8).  The DMMA k index of lane t in
+// k-step s is mapped to stage row k = (s/2)*8 + 2t + (s%2) (the same
+// permutation for A and B, so the sum is unchanged); with it, the 8 lanes of
+// each LDS.128 phase hit 8 different 16-B bank groups — conflict free.
+//
+// A (tensor) boxes, in f64 elements (one complex = 2):
+//   fiber-contiguous (n_left % 128 == 0): dims (16 [8 fibers], k-in-block,
+//     n_left/8 fiber groups, n_right, k blocks), box (16, 16, 16, 1, 1)
+//     → smem [fiber group][k][8 complex];
+//   k-contiguous (n_left == 1): dims (16 [8 k], fibers, K/8), box (16, 128, 2)
+//     → smem [k group][fiber][8 complex].
+// B (row-major factor): dims (16 [8 k], rows, K/8), box (16, 64, 2)
+//     → smem [k group][row][8 complex].
+#pragma once
+#include "kmb200_kernels.cuh"
+
+#include <cuda.h>
+
+namespace kmb {
+
+namespace tma {
+
+constexpr int BM = 128, BN = 64, BKS = 16, TSTAGES = 4, CONSUMERS = 8;
+constexpr int THREADS = 32 * CONSUMERS;
+constexpr int AHEAD = 2;  // k-blocks between a stage's load and its use
+constexpr int A_BYTES = BM * BKS * 16, B_BYTES = BN * BKS * 16, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM_BYTES = TSTAGES * STAGE_BYTES + 2 * TSTAGES * 8 + 1024;
+
+__device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "KMB_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra KMB_WAIT_%=;\n"
+      "}\n" ::"r"(su32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ double2 lds128(unsigned addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(m) : "memory");
+}
+__device__ __forceinline__ void load3(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];\n" ::"r"(su32(dst)),
+      "l"(m), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void load5(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2, int c3,
+                                      int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, "
+      "%7}], [%2];\n" ::"r"(su32(dst)),
+      "l"(m), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+
+}  // namespace tma
+
+template <bool KC, int OPK>
+__global__ void __launch_bounds__(tma::THREADS, 1)
+    mumode_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                      double2* __restrict__ out, int64_t M, int N, int K, int64_t nl, const OpDev op,
+                      const Split sp) {
+  using namespace tma;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TSTAGES * STAGE_BYTES);
+  uint64_t* empty = full + TSTAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TSTAGES; ++s) {
+      tma::mbar_init(&full[s], 1);
+      tma::mbar_init(&empty[s], CONSUMERS);
+    }
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+
+  const int nN = (N + BN - 1) / BN;
+  const int64_t tiles = ((M + BM - 1) / BM) * nN;
+  const int KT = (K + BKS - 1) / BKS;
+  const int64_t my_tiles = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total = my_tiles * KT;  // k-blocks this CTA consumes, over all its tiles
+
+  // one lane issues the loads of k-block q (tile q / KT of this CTA)
+  auto issue = [&](int64_t q) {
+    const int s = static_cast<int>(q % TSTAGES);
+    if (q >= TSTAGES) tma::mbar_wait(&empty[s], static_cast<unsigned>((q / TSTAGES - 1) & 1));
+    const int64_t tile = blockIdx.x + (q / KT) * gridDim.x;
+    const int kt = static_cast<int>(q % KT);
+    const int n0 = static_cast<int>(tile % nN) * BN;
+    const int64_t m0 = (tile / nN) * BM;
+    unsigned char* st = smem + s * STAGE_BYTES;
+    tma::mbar_expect_tx(&full[s], STAGE_BYTES);
+    const int k0 = kt * BKS;
+    if constexpr (KC) {
+      tma::load3(st, &mapA, &full[s], 0, static_cast<int>(m0), k0 / 8);
+    } else {
+      const int kb = k0 / sp.kcb;
+      tma::load5(st, &mapA, &full[s], 0, k0 - kb * sp.kcb, static_cast<int>((m0 % nl) / 8), static_cast<int>(m0 / nl),
+                 kb);
+    }
+    tma::load3(st + A_BYTES, &mapB, &full[s], 0, n0, k0 / 8);
+  };
+  const bool leader = (warp == 0 && lane == 0);
+  if (leader) {
+    tma::prefetch_map(&mapA);
+    tma::prefetch_map(&mapB);
+    for (int64_t q = 0; q < AHEAD && q < total; ++q) issue(q);
+  }
+
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+  const int gx = g ^ (2 * t);
+  // byte offsets of this lane's fragments inside a stage, for odd/even k-steps
+  constexpr unsigned A_I = KC ? 8 * 128 : 16 * 128;     // next 8-row MMA tile
+  constexpr unsigned A_KG = KC ? 128 * 128 : 8 * 128;   // next 8-k group
+  const unsigned a0 = KC ? (wm + g) * 128 + gx * 16 : ((wm / 8) * 16 + 2 * t) * 128 + gx * 16;
+  const unsigned a1 = KC ? (wm + g) * 128 + (gx ^ 1) * 16 : ((wm / 8) * 16 + 2 * t + 1) * 128 + (gx ^ 1) * 16;
+  constexpr unsigned B_J = 8 * 128, B_KG = 64 * 128;
+  const unsigned b0 = A_BYTES + (wn + g) * 128 + gx * 16;
+  const unsigned b1 = A_BYTES + (wn + g) * 128 + (gx ^ 1) * 16;
+
+  const unsigned sbase = tma::su32(smem);
+  int64_t q = 0;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int n0 = static_cast<int>(tile % nN) * BN;
+    const int64_t m0 = (tile / nN) * BM;
+    double cr[4][4][2], ci[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+
+    for (int kt = 0; kt < KT; ++kt, ++q) {
+      if (leader && q + AHEAD < total) issue(q + AHEAD);
+      const int s = static_cast<int>(q % TSTAGES);
+      tma::mbar_wait(&full[s], static_cast<unsigned>((q / TSTAGES) & 1));
+      const unsigned st = sbase + s * STAGE_BYTES;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const unsigned ao = ((ks & 1) ? a1 : a0) + (ks >> 1) * A_KG;
+        const unsigned bo = ((ks & 1) ? b1 : b0) + (ks >> 1) * B_KG;
+        double2 a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = tma::lds128(st + ao + i * A_I);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = tma::lds128(st + bo + j * B_J);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
+            dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
+          }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            dmma(cr[i][j][0], cr[i][j][1], a[i].y, negate(b[j].y));
+            dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
+          }
+      }
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(&empty[s]);
+    }
+
+    // epilogue (overlaps the producer's loads for the next tile)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t f = m0 + wm + i * 8 + g;
+      if (f >= M) continue;
+      const int64_t ob = KC ? f * N : (f % nl) + (f / nl) * nl * sp.ncb;
+      const int64_t cs = KC ? 1 : nl;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c8 = n0 + wn + j * 8;
+        const int nblk = KC ? 0 : c8 / sp.ncb;
+        const int64_t obj = ob + (KC ? 0 : nblk * sp.nbs) - static_cast<int64_t>(nblk) * sp.ncb * cs;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = c8 + 2 * t + h;
+          if (col >= N) continue;
+          const int64_t p = obj + static_cast<int64_t>(col) * cs;
+          double re = cr[i][j][h], im = ci[i][j][h];
+          if constexpr (OPK != KM_OP_NONE) apply_op<OPK>(op, p, re, im);
+          out[p] = make_double2(re, im);
+        }
+      }
+    }
+  }
+}
+
+// Host side: tensor maps + launch.  Returns -1 when the shape is not eligible
+// (the caller then uses the cp.async kernel).
+int launch_tma_c128(const void* u, const void* L, void* out, int64_t M, int N, int K, int64_t nl, const OpDev& op,
+                    const Split& sp, cudaStream_t st);
+
+}  // namespace kmb
