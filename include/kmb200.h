@@ -110,6 +110,19 @@ int km_mumode_split(const void* u, int u_dtype, const void* L, int L_dtype, void
                     int64_t out_block_stride, void* stream);
 
 /*
+ * complex64 x complex64 μ-mode product on the 5th-generation tensor cores
+ * (tcgen05.mma kind::tf32, TMEM accumulator, 3xTF32 split for fp32-level
+ * accuracy).  Same arguments as km_mumode plus a device workspace of at least
+ * km_tc_workspace_bytes(m, n_mu) bytes (the factor's split planes).  Shapes
+ * the kernel does not take (n_left > 1 with n_left % 64 != 0, n_mu % 4 != 0,
+ * a too-small workspace, KM_POLICY_NO_TMA) run the DMMA path instead.
+ */
+int km_tc_workspace_bytes(int64_t m, int64_t n_mu, size_t* bytes);
+int km_mumode_c64_tc(const void* u, const void* L, void* out, int64_t m, int64_t n_left,
+                     int64_t n_mu, int64_t n_right, void* workspace, size_t workspace_bytes,
+                     void* stream);
+
+/*
  * Tucker operator / exact propagator step (reference: tensor.tucker,
  * tensor.py:143-166; kron.step, kron.py:110-121; the Strang composition
  * problems.py:548-565 when pre/post are phases).

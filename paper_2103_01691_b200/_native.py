@@ -34,6 +34,8 @@ EXPORTS = (
     "km_tucker_workspace",
     "km_pointwise",
     "km_set_kernel_policy",
+    "km_tc_workspace_bytes",
+    "km_mumode_c64_tc",
 )
 
 
@@ -80,6 +82,10 @@ def _declare(lib):
         c_int, c_int, ctypes.POINTER(c_i64), ctypes.POINTER(c_vp), ctypes.POINTER(c_int),
         ctypes.POINTER(c_i64), ctypes.POINTER(c_sz),
     ]
+    lib.km_tc_workspace_bytes.restype = c_int
+    lib.km_tc_workspace_bytes.argtypes = [c_i64, c_i64, ctypes.POINTER(c_sz)]
+    lib.km_mumode_c64_tc.restype = c_int
+    lib.km_mumode_c64_tc.argtypes = [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_sz, c_vp]
     lib.km_set_kernel_policy.restype = c_int
     lib.km_set_kernel_policy.argtypes = [c_int]
     lib.km_pointwise.restype = c_int

@@ -130,11 +130,13 @@ def tucker_host_pipelined(host, u_dt, mats_dev, codes, rows, pre, post, out_shap
         with torch.cuda.stream(s_out):
             host_out_flat[lo:hi].copy_(out_dev[lo:hi], non_blocking=True)
 
+    from .tensor import launch_product
+
     def product(src, sdt, mu, m, shape, dst, op, lptr=None):
         nl, nr = prod(shape[:mu]), prod(shape[mu + 1:])
         lp = mats_dev[mu].data_ptr() if lptr is None else lptr
-        _native.check(lib.km_mumode(src.data_ptr(), dv.code(sdt), ctypes.c_void_p(lp), codes[mu], dst.data_ptr(),
-                                    m, nl, shape[mu], nr, None if op is None else ctypes.byref(op), stream_c))
+        launch_product(src.data_ptr(), dv.code(sdt), lp, codes[mu], dst.data_ptr(), m, nl, shape[mu], nr, op,
+                       stream_c, dev)
 
     # ---- phase 1: per input slab: H2D, pre op, directions 1..d-1
     for (start, size) in slabs:

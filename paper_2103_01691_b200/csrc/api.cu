@@ -10,6 +10,9 @@
 namespace kmb {
 
 extern bool g_tma_disabled;  // inst_tma_c128.cu
+size_t tc32_workspace_bytes(int64_t m, int64_t K);  // inst_tc32_c64.cu
+int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t nl, int64_t K, int64_t nr, void* ws,
+                    size_t ws_bytes, cudaStream_t st);
 thread_local char g_err[512] = "";
 
 int fail(int code, const char* fmt, ...) {
@@ -231,6 +234,24 @@ int km_mumode_split(const void* u, int u_dtype, const void* L, int L_dtype, void
   Split sp{in_block, in_block_stride, out_block, out_block_stride};
   return mumode_impl(u, u_dtype, L, L_dtype, out, m, n_left, n_mu, n_right, nullptr,
                      static_cast<cudaStream_t>(stream), &sp);
+}
+
+int km_tc_workspace_bytes(int64_t m, int64_t n_mu, size_t* bytes) {
+  if (!bytes || m < 1 || n_mu < 1) return fail(KM_EINVAL, "km_tc_workspace_bytes: bad arguments");
+  *bytes = tc32_workspace_bytes(m, n_mu);
+  return KM_OK;
+}
+
+int km_mumode_c64_tc(const void* u, const void* L, void* out, int64_t m, int64_t n_left, int64_t n_mu,
+                     int64_t n_right, void* workspace, size_t workspace_bytes, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!u || !L || !out) return fail(KM_EINVAL, "km_mumode_c64_tc: NULL pointer");
+  if (m < 1 || n_left < 1 || n_mu < 1 || n_right < 1) return fail(KM_EINVAL, "km_mumode_c64_tc: bad extents");
+  if (!g_tma_disabled) {
+    const int rc = launch_tc32_c64(u, L, out, m, n_left, n_mu, n_right, workspace, workspace_bytes, st);
+    if (rc >= 0) return rc;
+  }
+  return mumode_impl(u, KM_C64, L, KM_C64, out, m, n_left, n_mu, n_right, nullptr, st);
 }
 
 int km_tucker_workspace(int u_dtype, int d, const int64_t* dims, const void* const* mats, const int* mat_dtypes,

@@ -1,0 +1,103 @@
+// Host side of the tcgen05 complex64 μ-mode product: factor planes, TMA maps, launch.
+#include "kmb200_tc32.cuh"
+
+#include <cudaTypedefs.h>
+
+namespace kmb {
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn32() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool map_f32(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+             const cuuint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+  auto fn = encode_fn32();
+  if (!fn) return false;
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <bool KC>
+int launch(const CUtensorMap& ahi, const CUtensorMap& alo, const CUtensorMap& b, void* out, int64_t F, int m, int K,
+           int64_t nl, cudaStream_t st) {
+  auto kern = mumode_tc32_kernel<KC>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tc32::SMEM_BYTES);
+    if (e != cudaSuccess) return fail(KM_ECUDA, "cudaFuncSetAttribute(tc32): %s", cudaGetErrorString(e));
+    attr = true;
+  }
+  const int64_t fib_r = KC ? F : 2 * F;
+  const int64_t tiles = ((2 * m + tc32::BMR - 1) / tc32::BMR) * ((fib_r + tc32::BNR - 1) / tc32::BNR);
+  const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
+  kern<<<grid, tc32::THREADS, tc32::SMEM_BYTES, st>>>(ahi, alo, b, static_cast<float2*>(out), F, m, K, nl);
+  return check_launch("mumode_tc32_kernel");
+}
+
+}  // namespace
+
+size_t tc32_workspace_bytes(int64_t m, int64_t K) { return static_cast<size_t>(12 * m * K) * sizeof(float) + 256; }
+
+// Returns -1 when the shape is not eligible (caller falls back to the DMMA path).
+int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t nl, int64_t K, int64_t nr, void* ws,
+                    size_t ws_bytes, cudaStream_t st) {
+  const bool kc = (nl == 1);
+  const int64_t F = nl * nr;
+  if (!ws || ws_bytes < tc32_workspace_bytes(m, K)) return -1;
+  if ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(ws)) & 15) return -1;
+  if (K % 4 != 0 || m > (1 << 20) || K > (1 << 20)) return -1;
+  if (!kc && nl % 64 != 0) return -1;
+  if (F >= (int64_t(1) << 31)) return -1;
+  float* planes = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+  {
+    const int threads = 256;
+    int64_t blocks = (m * K + threads - 1) / threads;
+    if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
+    prep_planes_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(static_cast<const float2*>(L), planes,
+                                                                         static_cast<int>(m), static_cast<int>(K));
+    int rc = check_launch("prep_planes_kernel");
+    if (rc) return rc;
+  }
+  const int64_t kc_plane = 2 * m * 2 * K, mc_plane = 2 * m * K;
+  const int64_t KR = kc ? 2 * K : K;
+  const float* ahi = kc ? planes : planes + 2 * kc_plane;
+  const float* alo = kc ? planes + kc_plane : planes + 2 * kc_plane + mc_plane;
+  CUtensorMap mahi, malo, mb;
+  {
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(KR), static_cast<cuuint64_t>(2 * m), 1};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(KR) * 4, static_cast<cuuint64_t>(KR) * 4 * 2 * m};
+    cuuint32_t box[3] = {tc32::BKR, tc32::BMR, 1};
+    if (!map_f32(&mahi, ahi, 3, dims, strides, box) || !map_f32(&malo, alo, 3, dims, strides, box)) return -1;
+  }
+  if (kc) {
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(2 * K), static_cast<cuuint64_t>(F), 1};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(2 * K) * 4, static_cast<cuuint64_t>(2 * K) * 4 * F};
+    cuuint32_t box[3] = {tc32::BKR, tc32::BNR, 1};
+    if (!map_f32(&mb, u, 3, dims, strides, box)) return -1;
+    return launch<true>(mahi, malo, mb, out, F, static_cast<int>(m), static_cast<int>(K), nl, st);
+  }
+  cuuint64_t dims[5] = {32, static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(nl / 16), static_cast<cuuint64_t>(nr),
+                        1};
+  cuuint64_t strides[4] = {static_cast<cuuint64_t>(nl) * 8, 128, static_cast<cuuint64_t>(nl) * K * 8,
+                           static_cast<cuuint64_t>(nl) * K * 8 * nr};
+  cuuint32_t box[5] = {32, tc32::BKR, 4, 1, 1};
+  // MN-major tf32 operand: 32-B swizzle atoms (matches the BASE32B descriptor layout)
+  if (!map_f32(&mb, u, 5, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return -1;
+  return launch<false>(mahi, malo, mb, out, F, static_cast<int>(m), static_cast<int>(K), nl, st);
+}
+
+}  // namespace kmb

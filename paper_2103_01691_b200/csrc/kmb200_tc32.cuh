@@ -1,0 +1,323 @@
+// mumode_tc32_kernel — complex64 μ-mode product on the 5th-generation tensor
+// cores: tcgen05.mma kind::tf32 with the accumulator in TMEM, operands staged
+// by TMA, and a 3xTF32 split (hi*hi + lo*hi + hi*lo) that keeps the result at
+// fp32 accuracy (plain TF32 misses the 1e-5 complex64 parity bar by ~80x,
+// SURVEY §7.3).
+//
+// The factor E (m x n_mu) is the MMA's A operand (M side, 128 real rows per
+// tile = 64 complex rows), the tensor is the B operand (N side):
+//   * k-contiguous layout (direction 1, n_left == 1): the tensor's complex
+//     interleave lies along k, so both operands are real K-major matrices with
+//     K' = 2*n_mu: A = E_blk (2m x 2n_mu, rows 2n+c: [Er -Ei; Ei Er] blocks),
+//     B = U (fibers x 2n_mu).  D[2n+c][f] = (cr, ci)[f][n].
+//   * fiber-contiguous layout (n_left > 1): the interleave lies along the
+//     fibers, so B = U viewed as a real (2*fibers x n_mu) MN-major matrix and
+//     A = E' (2m x n_mu, rows 2n: Er, 2n+1: Ei).  D[2n+e][2f+c] = E_e*U_c;
+//     cr = D[2n][2f] - D[2n+1][2f+1], ci = D[2n][2f+1] + D[2n+1][2f] is formed
+//     in the epilogue with one lane shuffle.
+// Both are exactly 4 real multiply-adds per complex multiply-add (x3 for the
+// split).  E's hi/lo planes are prepared once per call (prep_planes_kernel);
+// the tensor tile is split in shared memory by four transform warps.
+//
+// Warp roles (10 warps): 0 TMA producer, 1 MMA issuer + TMEM owner,
+// 2-5 hi/lo transform, 6-9 epilogue (TMEM -> registers -> global).  The grid is
+// persistent; the two 128-column TMEM accumulators are double-buffered so the
+// epilogue of tile i overlaps the MMAs of tile i+1.
+#pragma once
+#include "kmb200_tma.cuh"
+
+namespace kmb {
+
+namespace tc32 {
+
+constexpr int BMR = 128;   // real rows of D per tile (64 complex rows of E)
+constexpr int BNR = 128;   // real columns of D per tile
+constexpr int BKR = 32;    // real k per stage (128 B of fp32)
+constexpr int ST = 3;      // pipeline stages
+constexpr int PLANE = BMR * BKR * 4;            // 16 KB: one 128 x 32 fp32 tile
+constexpr int STAGE_BYTES = 4 * PLANE;          // A hi, A lo, B raw->hi, B lo
+constexpr int TX_BYTES = 3 * PLANE;             // bytes TMA lands per stage
+constexpr int THREADS = 320;
+constexpr int SMEM_BYTES = ST * STAGE_BYTES + 1024 + 256;
+constexpr int TMEM_COLS = 256;
+
+// layout: 2 = SWIZZLE_128B (K-major operands), 1 = SWIZZLE_128B_BASE32B (the
+// only shared-memory layout the tensor core takes for MN-major tf32 operands)
+__device__ __forceinline__ uint64_t desc_sw128(unsigned saddr, unsigned lbo, unsigned sbo, unsigned layout = 2) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // descriptor version (sm_100)
+  d |= static_cast<uint64_t>(layout) << 61;
+  return d;
+}
+
+// kind::tf32, fp32 accumulate, A K-major, B K- or MN-major, M = 128, N = 128
+__host__ __device__ constexpr uint32_t idesc_tf32(bool b_mn_major) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((b_mn_major ? 1u : 0u) << 16) | ((BNR >> 3) << 17) |
+         ((BMR >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t dtmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(dtmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   tma::su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+__device__ __forceinline__ void ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float tf32_hi(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+}  // namespace tc32
+
+// E's split planes: [KC hi (2m x 2K)][KC lo][MC hi (2m x K)][MC lo], fp32 row-major.
+__global__ void prep_planes_kernel(const float2* __restrict__ L, float* __restrict__ planes, int m, int K) {
+  const int64_t kc = static_cast<int64_t>(2 * m) * (2 * K);
+  const int64_t mc = static_cast<int64_t>(2 * m) * K;
+  float* kc_hi = planes;
+  float* kc_lo = planes + kc;
+  float* mc_hi = planes + 2 * kc;
+  float* mc_lo = planes + 2 * kc + mc;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < static_cast<int64_t>(m) * K;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int n = static_cast<int>(idx / K), k = static_cast<int>(idx % K);
+    const float2 e = L[idx];
+    const float v[4] = {e.x, -e.y, e.y, e.x};  // E_blk[2n+r][2k+c]: [[Er, -Ei], [Ei, Er]]
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = q >> 1, c = q & 1;
+      const int64_t o = static_cast<int64_t>(2 * n + r) * (2 * K) + 2 * k + c;
+      const float hi = tc32::tf32_hi(v[q]);
+      kc_hi[o] = hi;
+      kc_lo[o] = v[q] - hi;
+    }
+    const float w[2] = {e.x, e.y};  // E'[2n+e][k]
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int64_t o = static_cast<int64_t>(2 * n + q) * K + k;
+      const float hi = tc32::tf32_hi(w[q]);
+      mc_hi[o] = hi;
+      mc_lo[o] = w[q] - hi;
+    }
+  }
+}
+
+template <bool KC>
+__global__ void __launch_bounds__(tc32::THREADS, 1)
+    mumode_tc32_kernel(const __grid_constant__ CUtensorMap mapAhi, const __grid_constant__ CUtensorMap mapAlo,
+                       const __grid_constant__ CUtensorMap mapB, float2* __restrict__ out, int64_t F, int m, int K,
+                       int64_t nl) {
+  using namespace tc32;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * STAGE_BYTES);
+  uint64_t* ready = full + ST;
+  uint64_t* empty = ready + ST;
+  uint64_t* tfull = empty + ST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      tma::mbar_init(&full[s], 1);
+      tma::mbar_init(&ready[s], 4);
+      tma::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tma::mbar_init(&tfull[b], 1);
+      tma::mbar_init(&tempty[b], 4);
+    }
+    tma::fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tma::su32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int64_t fib_r = KC ? F : 2 * F;               // real columns of B
+  const int nE = (2 * m + BMR - 1) / BMR;             // tiles along E's real rows
+  const int64_t nF = (fib_r + BNR - 1) / BNR;         // tiles along the real columns
+  const int64_t tiles = nE * nF;
+  const int KR = KC ? 2 * K : K;                      // real contraction length
+  const int KT = (KR + BKR - 1) / BKR;
+  const int64_t my_tiles = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const unsigned sbase = tma::su32(smem);
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      tma::prefetch_map(&mapAhi);
+      tma::prefetch_map(&mapAlo);
+      tma::prefetch_map(&mapB);
+      int64_t q = 0;
+      for (int64_t it = 0; it < my_tiles; ++it) {
+        const int64_t tile = blockIdx.x + it * gridDim.x;
+        const int e0 = static_cast<int>(tile % nE) * BMR;
+        const int64_t c0 = (tile / nE) * BNR;
+        for (int kt = 0; kt < KT; ++kt, ++q) {
+          const int s = static_cast<int>(q % ST);
+          if (q >= ST) tma::mbar_wait(&empty[s], static_cast<unsigned>((q / ST - 1) & 1));
+          unsigned char* st = smem + s * STAGE_BYTES;
+          tma::mbar_expect_tx(&full[s], TX_BYTES);
+          const int k0 = kt * BKR;
+          tma::load3(st, &mapAhi, &full[s], k0, e0, 0);
+          tma::load3(st + PLANE, &mapAlo, &full[s], k0, e0, 0);
+          if constexpr (KC) {
+            tma::load3(st + 2 * PLANE, &mapB, &full[s], k0, static_cast<int>(c0), 0);
+          } else {
+            const int64_t f0 = c0 / 2;  // fibers; the tile lies inside one n_left slab
+            tma::load5(st + 2 * PLANE, &mapB, &full[s], 0, k0, static_cast<int>((f0 % nl) / 16),
+                       static_cast<int>(f0 / nl), 0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(!KC);
+      int64_t q = 0;
+      for (int64_t it = 0; it < my_tiles; ++it) {
+        const int b = static_cast<int>(it & 1);
+        if (it >= 2) tma::mbar_wait(&tempty[b], static_cast<unsigned>(((it >> 1) - 1) & 1));
+        fence_after();
+        const uint32_t d = tmem + b * BNR;
+        for (int kt = 0; kt < KT; ++kt, ++q) {
+          const int s = static_cast<int>(q % ST);
+          tma::mbar_wait(&ready[s], static_cast<unsigned>((q / ST) & 1));
+          fence_after();
+          const unsigned st = sbase + s * STAGE_BYTES;
+#pragma unroll
+          for (int ks = 0; ks < BKR / 8; ++ks) {
+            // A (E planes): K-major SW128, 8 k = 32 B per step inside the 128-B row
+            const uint64_t ahi = desc_sw128(st + ks * 32, 16, 1024);
+            const uint64_t alo = desc_sw128(st + PLANE + ks * 32, 16, 1024);
+            uint64_t bhi, blo;
+            if constexpr (KC) {  // K-major like A
+              bhi = desc_sw128(st + 2 * PLANE + ks * 32, 16, 1024);
+              blo = desc_sw128(st + 3 * PLANE + ks * 32, 16, 1024);
+            } else {  // MN-major: 32-float column chunks 4096 B apart (LBO), 4-k groups 512 B apart (SBO)
+              bhi = desc_sw128(st + 2 * PLANE + ks * 1024, 4096, 512, 1);
+              blo = desc_sw128(st + 3 * PLANE + ks * 1024, 4096, 512, 1);
+            }
+            const uint32_t acc = (kt | ks) ? 1u : 0u;
+            mma_tf32(d, ahi, bhi, idesc, acc);
+            mma_tf32(d, alo, bhi, idesc, 1u);
+            mma_tf32(d, ahi, blo, idesc, 1u);
+          }
+          commit(&empty[s]);
+        }
+        commit(&tfull[b]);
+      }
+    }
+  } else if (warp < 6) {
+    // ------------------------------------------------------------ hi/lo split of the tensor tile
+    const int tt = threadIdx.x - 64;  // 0..127
+    int64_t q = 0;
+    for (int64_t it = 0; it < my_tiles; ++it) {
+      for (int kt = 0; kt < KT; ++kt, ++q) {
+        const int s = static_cast<int>(q % ST);
+        tma::mbar_wait(&full[s], static_cast<unsigned>((q / ST) & 1));
+        float4* raw = reinterpret_cast<float4*>(smem + s * STAGE_BYTES + 2 * PLANE);
+        float4* lo = reinterpret_cast<float4*>(smem + s * STAGE_BYTES + 3 * PLANE);
+#pragma unroll
+        for (int j = 0; j < PLANE / 16 / 128; ++j) {
+          const int idx = tt + 128 * j;
+          float4 x = raw[idx];
+          float4 h = make_float4(tc32::tf32_hi(x.x), tc32::tf32_hi(x.y), tc32::tf32_hi(x.z), tc32::tf32_hi(x.w));
+          raw[idx] = h;
+          lo[idx] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) tma::mbar_arrive(&ready[s]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
+    const int row = quarter * 32 + lane;
+    for (int64_t it = 0; it < my_tiles; ++it) {
+      const int64_t tile = blockIdx.x + it * gridDim.x;
+      const int e0 = static_cast<int>(tile % nE) * BMR;
+      const int64_t c0 = (tile / nE) * BNR;
+      const int b = static_cast<int>(it & 1);
+      tma::mbar_wait(&tfull[b], static_cast<unsigned>((it >> 1) & 1));
+      fence_after();
+      const int er = e0 + row;  // real row of E: n = er / 2, part = er & 1
+      const int n = er >> 1, part = er & 1;
+      float* outf = reinterpret_cast<float*>(out);
+#pragma unroll 1
+      for (int ch = 0; ch < BNR / 32; ++ch) {
+        float v[32];
+        ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + b * BNR + ch * 32, v);
+        if constexpr (KC) {
+          // D[2n+part][f] = part ? ci : cr of output (f, n); out[f*m + n]
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int64_t f = c0 + ch * 32 + j;
+            if (n < m && f < F) outf[2 * (f * m + n) + part] = v[j];
+          }
+        } else {
+          // columns 2f+c; cr = D[2n][2f] - D[2n+1][2f+1], ci = D[2n][2f+1] + D[2n+1][2f]
+          const int64_t fb = (c0 + ch * 32) / 2;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float x = __shfl_xor_sync(0xffffffffu, v[2 * j + 1], 1);
+            const float val = part ? v[2 * j] + x : v[2 * j] - x;
+            const int64_t f = fb + j;
+            if (n < m && f < F) {
+              const int64_t o = (f % nl) + (f / nl) * nl * m + static_cast<int64_t>(n) * nl;
+              outf[2 * o + part] = val;
+            }
+          }
+        }
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(&tempty[b]);
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
+}  // namespace kmb

@@ -143,6 +143,28 @@ def _tensor_on_device(op, dtype, dev):
     return dv.to_device(op.obj, dtype, dev)
 
 
+_TC_WORKSPACE = {}
+
+
+def launch_product(src_ptr, src_code, mat_ptr, mat_code, dst_ptr, m, nl, nmu, nr, op, stream, dev):
+    """One μ-mode product through the C ABI: complex64 x complex64 on the tcgen05
+    (TF32x3) kernel, everything else on the DMMA kernels."""
+    lib = _native.lib()
+    if src_code == _native.KM_C64 and mat_code == _native.KM_C64 and op is None:
+        need = ctypes.c_size_t(0)
+        _native.check(lib.km_tc_workspace_bytes(m, nmu, ctypes.byref(need)))
+        key = str(dev)
+        buf = _TC_WORKSPACE.get(key)
+        if buf is None or buf.numel() < need.value:
+            buf = dv.torch.empty(need.value, dtype=dv.torch.uint8, device=dev)
+            _TC_WORKSPACE[key] = buf
+        _native.check(lib.km_mumode_c64_tc(src_ptr, mat_ptr, dst_ptr, m, nl, nmu, nr, buf.data_ptr(),
+                                           buf.numel(), stream))
+        return
+    _native.check(lib.km_mumode(src_ptr, src_code, mat_ptr, mat_code, dst_ptr, m, nl, nmu, nr,
+                                None if op is None else ctypes.byref(op), stream))
+
+
 def run_tucker(u, mats, pre=None, post=None, out_dtype=None, keepalive=()):
     """Core device driver: ``post(pre(u) x_1 mats[0] ... x_d mats[d-1])``.
 
@@ -199,7 +221,10 @@ def run_tucker(u, mats, pre=None, post=None, out_dtype=None, keepalive=()):
     lib = _native.lib()
     out = dv.fortran_empty(out_shape, dv.torch_dtype(cdt), dev)
     stream = dv.stream_ptr(dev)
-    if d <= _native.MAX_D:
+    c64 = np.dtype(np.complex64)
+    tc_loop = (u_dt == c64 and pre is None and post is None
+               and all(c == _native.KM_C64 for t, c in zip(mats_dev, codes) if t is not None))
+    if d <= _native.MAX_D and not tc_loop:
         c_dims = (ctypes.c_int64 * d)(*uo.shape)
         c_mats = (ctypes.c_void_p * d)(*[None if t is None else t.data_ptr() for t in mats_dev])
         c_codes = (ctypes.c_int * d)(*codes)
@@ -233,12 +258,8 @@ def run_tucker(u, mats, pre=None, post=None, out_dtype=None, keepalive=()):
             shape_new = list(shape)
             shape_new[mu] = rows[mu]
             dst = out if idx == len(active) - 1 else dv.fortran_empty(shape_new, dv.torch_dtype(new_dt), dev)
-            _native.check(
-                lib.km_mumode(
-                    src.data_ptr(), dv.code(src_dt), mats_dev[mu].data_ptr(), codes[mu], dst.data_ptr(),
-                    rows[mu], prod(shape[:mu]), shape[mu], prod(shape[mu + 1:]), None, stream,
-                )
-            )
+            launch_product(src.data_ptr(), dv.code(src_dt), mats_dev[mu].data_ptr(), codes[mu], dst.data_ptr(),
+                           rows[mu], prod(shape[:mu]), shape[mu], prod(shape[mu + 1:]), None, stream, dev)
             src, src_dt, shape = dst, new_dt, shape_new
     return _finish(uo, out, result, cdt)
 

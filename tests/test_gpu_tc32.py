@@ -1,0 +1,54 @@
+"""GPU: complex64 products on the tcgen05 (kind::tf32, 3xTF32 split) kernel against
+the oracle (the reference's own complex64 arithmetic) and the complex128 oracle."""
+
+import numpy as np
+import pytest
+
+import paper_2103_01691_b200 as km
+from oracle import kronmode_oracle as orc
+from paper_2103_01691_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+
+def crand(rng, shape, dt=np.complex64):
+    return np.asfortranarray((rng.standard_normal(shape) + 1j * rng.standard_normal(shape)).astype(dt))
+
+
+CASES = [((128, 128, 128), 1, 128), ((128, 128, 128), 2, 128), ((128, 128, 128), 3, 128),
+         ((200, 96, 64), 1, 200), ((200, 96, 64), 3, 64), ((128, 128, 128), 3, 100),
+         ((256, 256, 256), 1, 256), ((256, 256, 256), 2, 256), ((256, 256, 256), 3, 256)]
+
+
+@pytest.mark.parametrize("shape,mu,m", CASES)
+def test_c64_products_vs_oracle(shape, mu, m):
+    rng = np.random.default_rng(sum(shape) + mu + m)
+    u = crand(rng, shape)
+    mat = ((rng.standard_normal((m, shape[mu - 1])) + 1j * rng.standard_normal((m, shape[mu - 1])))
+           / np.sqrt(shape[mu - 1])).astype(np.complex64)
+    got = km.mu_mode_product(u, mat, mu)
+    assert got.dtype == np.complex64
+    want64 = orc.mu_mode_product(u, mat, mu)
+    want128 = orc.mu_mode_product(u.astype(np.complex128), mat.astype(np.complex128), mu)
+    e64, e128 = orc.rel_l2(got, want64), orc.rel_l2(got, want128)
+    assert e64 <= 1e-5, e64
+    assert e128 <= 1e-5, e128
+
+
+def test_c64_step_256_vs_oracle_and_dmma():
+    n = 256
+    rng = np.random.default_rng(0)
+    u = crand(rng, (n,) * 3)
+    d2 = km.heat_factors(n, 2).factors[0]
+    c128 = km.prepare(km.KroneckerOp((1j * d2,) * 3), 0.01)
+    cache = km.PropagatorCache(0.01, tuple(e.astype(np.complex64) for e in c128.exps))
+    got = km.step(cache, u)
+    want = orc.step(cache.exps, u)
+    assert orc.rel_l2(got, want) <= 1e-5
+    lib = _native.lib()
+    try:
+        _native.check(lib.km_set_kernel_policy(_native.POLICY_NO_TMA))
+        dmma = km.step(cache, u)
+    finally:
+        _native.check(lib.km_set_kernel_policy(_native.POLICY_AUTO))
+    assert orc.rel_l2(got, dmma) <= 1e-5
