@@ -60,7 +60,7 @@ int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t 
   if (!ws || ws_bytes < tc32_workspace_bytes(m, K)) return -1;
   if ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(ws)) & 15) return -1;
   if (K % 4 != 0 || m > (1 << 20) || K > (1 << 20)) return -1;
-  if (!kc && nl % 64 != 0) return -1;
+  if (!kc && nl % (tc32::BNR / 2) != 0) return -1;  // a tile's fibers lie inside one slab
   if (F >= (int64_t(1) << 31)) return -1;
   float* planes = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
   {
@@ -81,20 +81,22 @@ int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t 
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(KR), static_cast<cuuint64_t>(2 * m), 1};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(KR) * 4, static_cast<cuuint64_t>(KR) * 4 * 2 * m};
     cuuint32_t box[3] = {tc32::BKR, tc32::BMR, 1};
-    if (!map_f32(&mahi, ahi, 3, dims, strides, box) || !map_f32(&malo, alo, 3, dims, strides, box)) return -1;
+    if (!map_f32(&mahi, ahi, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B) ||
+        !map_f32(&malo, alo, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B))
+      return -1;
   }
   if (kc) {
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(2 * K), static_cast<cuuint64_t>(F), 1};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(2 * K) * 4, static_cast<cuuint64_t>(2 * K) * 4 * F};
     cuuint32_t box[3] = {tc32::BKR, tc32::BNR, 1};
-    if (!map_f32(&mb, u, 3, dims, strides, box)) return -1;
+    if (!map_f32(&mb, u, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B)) return -1;
     return launch<true>(mahi, malo, mb, out, F, static_cast<int>(m), static_cast<int>(K), nl, st);
   }
   cuuint64_t dims[5] = {32, static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(nl / 16), static_cast<cuuint64_t>(nr),
                         1};
   cuuint64_t strides[4] = {static_cast<cuuint64_t>(nl) * 8, 128, static_cast<cuuint64_t>(nl) * K * 8,
                            static_cast<cuuint64_t>(nl) * K * 8 * nr};
-  cuuint32_t box[5] = {32, tc32::BKR, 4, 1, 1};
+  cuuint32_t box[5] = {32, tc32::BKR, tc32::BNR / 32, 1, 1};
   // MN-major tf32 operand: 32-B swizzle atoms (matches the BASE32B descriptor layout)
   if (!map_f32(&mb, u, 5, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return -1;
   return launch<false>(mahi, malo, mb, out, F, static_cast<int>(m), static_cast<int>(K), nl, st);

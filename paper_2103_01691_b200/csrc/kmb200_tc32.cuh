@@ -31,19 +31,23 @@ namespace kmb {
 namespace tc32 {
 
 constexpr int BMR = 128;   // real rows of D per tile (64 complex rows of E)
-constexpr int BNR = 128;   // real columns of D per tile
-constexpr int BKR = 32;    // real k per stage (128 B of fp32)
-constexpr int ST = 3;      // pipeline stages
-constexpr int PLANE = BMR * BKR * 4;            // 16 KB: one 128 x 32 fp32 tile
-constexpr int STAGE_BYTES = 4 * PLANE;          // A hi, A lo, B raw->hi, B lo
-constexpr int TX_BYTES = 3 * PLANE;             // bytes TMA lands per stage
+constexpr int BNR = 256;   // real columns of D per tile (one N=256 MMA)
+constexpr int BKR = 16;    // real k per stage (64 B of fp32: SWIZZLE_64B K-major rows)
+constexpr int ST = 4;      // pipeline stages
+constexpr int PLANE_A = BMR * BKR * 4;          // 8 KB: 128 x 16 fp32 (E hi or lo)
+constexpr int PLANE_B = BNR * BKR * 4;          // 16 KB: 256 x 16 fp32 (tensor raw->hi or lo)
+constexpr int OFF_ALO = PLANE_A, OFF_B = 2 * PLANE_A, OFF_BLO = 2 * PLANE_A + PLANE_B;
+constexpr int STAGE_BYTES = 2 * PLANE_A + 2 * PLANE_B;
+constexpr int TX_BYTES = 2 * PLANE_A + PLANE_B;  // bytes TMA lands per stage
 constexpr int THREADS = 320;
-constexpr int SMEM_BYTES = ST * STAGE_BYTES + 1024 + 256;
-constexpr int TMEM_COLS = 256;
+constexpr int XPITCH = 34;  // epilogue transpose buffer row pitch (floats): conflict-free both ways
+constexpr int XBUF = 16 * XPITCH * 4;  // per epilogue warp
+constexpr int SMEM_BYTES = ST * STAGE_BYTES + 4 * XBUF + 1024 + 256;
+constexpr int TMEM_COLS = 512;  // two 256-column accumulators
 
-// layout: 2 = SWIZZLE_128B (K-major operands), 1 = SWIZZLE_128B_BASE32B (the
-// only shared-memory layout the tensor core takes for MN-major tf32 operands)
-__device__ __forceinline__ uint64_t desc_sw128(unsigned saddr, unsigned lbo, unsigned sbo, unsigned layout = 2) {
+// layout: 4 = SWIZZLE_64B (K-major operands, 64-B rows), 1 = SWIZZLE_128B_BASE32B
+// (the only shared-memory layout the tensor core takes for MN-major tf32 operands)
+__device__ __forceinline__ uint64_t desc_sw(unsigned saddr, unsigned lbo, unsigned sbo, unsigned layout) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
   d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
@@ -147,6 +151,7 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
   uint64_t* tfull = empty + ST;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* xbuf_all = reinterpret_cast<float*>(smem + ST * STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -198,12 +203,12 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
           tma::mbar_expect_tx(&full[s], TX_BYTES);
           const int k0 = kt * BKR;
           tma::load3(st, &mapAhi, &full[s], k0, e0, 0);
-          tma::load3(st + PLANE, &mapAlo, &full[s], k0, e0, 0);
+          tma::load3(st + OFF_ALO, &mapAlo, &full[s], k0, e0, 0);
           if constexpr (KC) {
-            tma::load3(st + 2 * PLANE, &mapB, &full[s], k0, static_cast<int>(c0), 0);
+            tma::load3(st + OFF_B, &mapB, &full[s], k0, static_cast<int>(c0), 0);
           } else {
             const int64_t f0 = c0 / 2;  // fibers; the tile lies inside one n_left slab
-            tma::load5(st + 2 * PLANE, &mapB, &full[s], 0, k0, static_cast<int>((f0 % nl) / 16),
+            tma::load5(st + OFF_B, &mapB, &full[s], 0, k0, static_cast<int>((f0 % nl) / 16),
                        static_cast<int>(f0 / nl), 0);
           }
         }
@@ -226,16 +231,16 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
           const unsigned st = sbase + s * STAGE_BYTES;
 #pragma unroll
           for (int ks = 0; ks < BKR / 8; ++ks) {
-            // A (E planes): K-major SW128, 8 k = 32 B per step inside the 128-B row
-            const uint64_t ahi = desc_sw128(st + ks * 32, 16, 1024);
-            const uint64_t alo = desc_sw128(st + PLANE + ks * 32, 16, 1024);
+            // A (E planes): K-major SW64 (8 rows x 64 B atoms, 512 B apart); 8 k = 32 B per step
+            const uint64_t ahi = desc_sw(st + ks * 32, 16, 512, 4);
+            const uint64_t alo = desc_sw(st + OFF_ALO + ks * 32, 16, 512, 4);
             uint64_t bhi, blo;
             if constexpr (KC) {  // K-major like A
-              bhi = desc_sw128(st + 2 * PLANE + ks * 32, 16, 1024);
-              blo = desc_sw128(st + 3 * PLANE + ks * 32, 16, 1024);
-            } else {  // MN-major: 32-float column chunks 4096 B apart (LBO), 4-k groups 512 B apart (SBO)
-              bhi = desc_sw128(st + 2 * PLANE + ks * 1024, 4096, 512, 1);
-              blo = desc_sw128(st + 3 * PLANE + ks * 1024, 4096, 512, 1);
+              bhi = desc_sw(st + OFF_B + ks * 32, 16, 512, 4);
+              blo = desc_sw(st + OFF_BLO + ks * 32, 16, 512, 4);
+            } else {  // MN-major: 32-float column chunks 2048 B apart (LBO), 4-k groups 512 B apart (SBO)
+              bhi = desc_sw(st + OFF_B + ks * 1024, 2048, 512, 1);
+              blo = desc_sw(st + OFF_BLO + ks * 1024, 2048, 512, 1);
             }
             const uint32_t acc = (kt | ks) ? 1u : 0u;
             mma_tf32(d, ahi, bhi, idesc, acc);
@@ -255,10 +260,10 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
       for (int kt = 0; kt < KT; ++kt, ++q) {
         const int s = static_cast<int>(q % ST);
         tma::mbar_wait(&full[s], static_cast<unsigned>((q / ST) & 1));
-        float4* raw = reinterpret_cast<float4*>(smem + s * STAGE_BYTES + 2 * PLANE);
-        float4* lo = reinterpret_cast<float4*>(smem + s * STAGE_BYTES + 3 * PLANE);
+        float4* raw = reinterpret_cast<float4*>(smem + s * STAGE_BYTES + OFF_B);
+        float4* lo = reinterpret_cast<float4*>(smem + s * STAGE_BYTES + OFF_BLO);
 #pragma unroll
-        for (int j = 0; j < PLANE / 16 / 128; ++j) {
+        for (int j = 0; j < PLANE_B / 16 / 128; ++j) {
           const int idx = tt + 128 * j;
           float4 x = raw[idx];
           float4 h = make_float4(tc32::tf32_hi(x.x), tc32::tf32_hi(x.y), tc32::tf32_hi(x.z), tc32::tf32_hi(x.w));
@@ -296,18 +301,29 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
             if (n < m && f < F) outf[2 * (f * m + n) + part] = v[j];
           }
         } else {
-          // columns 2f+c; cr = D[2n][2f] - D[2n+1][2f+1], ci = D[2n][2f+1] + D[2n+1][2f]
-          const int64_t fb = (c0 + ch * 32) / 2;
+          // columns 2f+c; cr = D[2n][2f] - D[2n+1][2f+1], ci = D[2n][2f+1] + D[2n+1][2f].
+          // Lane 2n'+part ends up with 16 fibers of output row n'; a transpose through
+          // shared memory gives lane 2f+part the 16 rows of fiber f, so every store
+          // instruction writes 128 contiguous bytes (16 fibers x complex64 of one row).
+          float* xb = xbuf_all + (warp - 6) * (XBUF / 4);
+          const int np = lane >> 1;
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const float x = __shfl_xor_sync(0xffffffffu, v[2 * j + 1], 1);
-            const float val = part ? v[2 * j] + x : v[2 * j] - x;
-            const int64_t f = fb + j;
-            if (n < m && f < F) {
-              const int64_t o = (f % nl) + (f / nl) * nl * m + static_cast<int64_t>(n) * nl;
-              outf[2 * o + part] = val;
-            }
+            xb[np * XPITCH + 2 * j + part] = part ? v[2 * j] + x : v[2 * j] - x;
           }
+          __syncwarp();
+          // the tile's fibers lie inside one n_left slab: one division per tile
+          const int64_t ft = c0 / 2 + ch * 16, r = ft / nl;
+          const int64_t fl = ft - r * nl + (lane >> 1);
+          const int nbase = (e0 >> 1) + quarter * 16;
+          const bool fok = ft + (lane >> 1) < F;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int nn = nbase + j;
+            if (fok && nn < m) outf[2 * (fl + r * nl * m + static_cast<int64_t>(nn) * nl) + part] = xb[j * XPITCH + lane];
+          }
+          __syncwarp();
         }
       }
       fence_before();
