@@ -269,7 +269,7 @@ def run_ours(args):
             achieved = flop_launch / (avg_ms * 1e-3) / 1e12
             roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak, "traffic": traffic_from_profile(),
-                    "kernel": "mumode_kernel (DMMA.8x8x4, complex128)",
+                    "kernel": "mumode_tma_kernel (TMA + mbarrier ring, DMMA.8x8x4, complex128)",
                     "algorithmic_per_launch": f"{flop_launch} flop (8 * 256^4)",
                     "launch_ms": per_mode, "peak_source": peak_src}
 

@@ -1,0 +1,51 @@
+"""Run under torchrun (any world size): the NCCL slab stepper against a single-GPU
+reference computed on rank 0.  Exits non-zero on a parity failure.
+
+    torchrun --nproc-per-node P --master-addr 127.0.0.1 --master-port 29511 tools/slab_check.py [n] [steps]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as tdist  # noqa: E402
+
+import paper_2103_01691_b200 as km  # noqa: E402
+from paper_2103_01691_b200 import _device as dv, dist  # noqa: E402
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+    steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    ngpu = torch.cuda.device_count()
+    dev = torch.device("cuda", local % ngpu)
+    torch.cuda.set_device(dev)
+    tdist.init_process_group("nccl", device_id=dev)
+    rank, world = tdist.get_rank(), tdist.get_world_size()
+    rng = np.random.default_rng(0)
+    u = np.asfortranarray(rng.standard_normal((n,) * 3) + 1j * rng.standard_normal((n,) * 3))
+    d2 = km.heat_factors(n, 2).factors[0]
+    cache = km.prepare(km.KroneckerOp((1j * d2,) * 3), 0.01)
+    st = dist.SlabStepper.from_global(u, cache, dev)
+    for _ in range(steps):
+        st.step()
+    torch.cuda.synchronize()
+    mine = dv.to_host(st.local_state())
+    ref = dist.LocalStepper(dv.to_device(u, np.complex128, dev), cache.device_exps((np.complex128,) * 3, dev))
+    for _ in range(steps):
+        ref.step()
+    want = dv.to_host(ref.state)
+    want_slab = st.plan.slab_a(want, rank) if st.layout == "A" else st.plan.slab_b(want, rank)
+    err = float(np.linalg.norm((mine - want_slab).ravel()) / np.linalg.norm(want_slab.ravel()))
+    errs = torch.tensor([err], device=dev)
+    tdist.all_reduce(errs, op=tdist.ReduceOp.MAX)
+    if rank == 0:
+        print(f"slab_check world={world} n={n} steps={steps} layout={st.layout} max_rel_l2={errs.item():.3e}")
+    tdist.destroy_process_group()
+    sys.exit(0 if errs.item() <= 1e-12 else 1)
+
+
+if __name__ == "__main__":
+    main()
