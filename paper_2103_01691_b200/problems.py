@@ -91,7 +91,7 @@ def _check_weights(weights, shape):
 def _strang_dtype(psi_dtype, cache):
     # the reference's phase multiplies by a complex128 factor (problems.py:545),
     # so the state leaves the nonlinear half step as complex128 whatever came in
-    return np.result_type(psi_dtype, np.complex128, *(e.dtype for e in cache.exps))
+    return np.result_type(psi_dtype, np.complex128, *cache.exp_dtypes())
 
 
 def gpe_strang_step(linear_cache, weights, psi, tau, _timer=None):
@@ -169,14 +169,20 @@ def tdpot_strang_step(linear_cache, x_nodes, psi, t, tau, direction=3):
     return run_tucker(state, mats, pre=pre, post=post, out_dtype=out_dtype, keepalive=(f_a, f_b))
 
 
-def magnus_midpoint_step(factors_of_t, u, t, tau):
+def magnus_midpoint_step(factors_of_t, u, t, tau, device_expm=False):
     """Exponential midpoint rule ``u <- exp(tau * M(t + tau/2)) u`` (problems.py:374-382).
 
-    The midpoint exponentials are host scipy ``expm`` (as the reference); the
-    step is the device Tucker product.  Host work for the next call overlaps
-    the device work of this one because device launches are asynchronous.
+    By default the midpoint exponentials are host scipy ``expm``, as in the
+    reference; the step is the device Tucker product, and host work for the
+    next call overlaps the device work of this one because device launches
+    are asynchronous.  ``device_expm=True`` takes the exponentials on the GPU
+    as well (:mod:`expm`).
     """
     op = factors_of_t(t + 0.5 * tau)
+    if device_expm:
+        from .expm import prepare_device
+
+        return step(prepare_device(op, tau), u)
     return step(prepare(op, tau), u)
 
 
