@@ -193,6 +193,52 @@ def config5(budget, n=512):
             "cpu_reps": kk, "speedup": cpu_ms / ms, "parity_rel_l2": orc.rel_l2(got, want)}
 
 
+def config_magnus(budget, k=256, steps=4):
+    """Extra: HKMP Magnus midpoint steps, host vs device exponentials."""
+    from paper_2103_01691_b200.problems import hkmp_factors, schrodinger_initial_state
+
+    b = km.hermite_basis(k)
+    psi0 = schrodinger_initial_state((b.nodes,) * 3)
+    c0 = dv.to_device(km.forward_transform((b,) * 3, psi0), np.complex128, DEV)
+    tau = 1.0 / 32
+
+    def run(device_expm):
+        u = c0
+        for s in range(steps):
+            u = km.magnus_midpoint_step(lambda t: hkmp_factors(b, t), u, s * tau, tau, device_expm=device_expm)
+        return u
+
+    import time as _t
+
+    for flag in (False, True):
+        run(flag)
+    torch.cuda.synchronize()
+    t0 = _t.perf_counter()
+    host = run(False)
+    torch.cuda.synchronize()
+    ms_host = (_t.perf_counter() - t0) * 1e3 / steps
+    t0 = _t.perf_counter()
+    devr = run(True)
+    torch.cuda.synchronize()
+    ms_dev = (_t.perf_counter() - t0) * 1e3 / steps
+    c0h = dv.to_host(c0)
+
+    def cpu_run():
+        from paper_2103_01691_b200.linalg import matexp
+
+        u = c0h
+        for s in range(steps):
+            op = hkmp_factors(b, (s + 0.5) * tau)
+            u = orc.step([matexp(tau * a) for a in op.factors], u)
+        return u
+
+    cpu_ms, kk = cpu_time(cpu_run, budget, 2)
+    return {"config": f"extra: HKMP Magnus midpoint step k={k} c128 (wall clock per step incl. exponentials)",
+            "gpu_ms_host_expm": ms_host, "gpu_ms_device_expm": ms_dev, "cpu_ms": cpu_ms / steps, "cpu_reps": kk,
+            "speedup_device_expm": cpu_ms / steps / ms_dev,
+            "parity_rel_l2_device_vs_host_expm": orc.rel_l2(dv.to_host(devr), dv.to_host(host))}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cpu-budget", type=float, default=20.0)
@@ -201,7 +247,7 @@ def main():
     args = ap.parse_args()
     cores = os.cpu_count() or 1
     res = {"cores": cores, "configs": []}
-    fns = {"1": config1, "2": config2, "3": config3, "4": config4, "5": config5}
+    fns = {"1": config1, "2": config2, "3": config3, "4": config4, "5": config5, "m": config_magnus}
     with threadpool_limits(limits=cores):
         for key in args.only:
             t0 = time.time()
