@@ -32,10 +32,10 @@ bool make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims
   return r == CUDA_SUCCESS;
 }
 
-template <bool KC, int OPK>
+template <bool KC, int OPK, bool CL>
 int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* out, int64_t M, int N, int K, int64_t nl,
            const OpDev& op, const Split& sp, cudaStream_t st) {
-  auto kern = mumode_tma_kernel<KC, OPK>;
+  auto kern = mumode_tma_kernel<KC, OPK, CL>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tma::SMEM_BYTES);
@@ -53,7 +53,7 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* out, int64_t M, i
 bool g_tma_disabled = false;
 
 int launch_tma_c128(const void* u, const void* L, void* out, int64_t M, int N, int K, int64_t nl, const OpDev& op,
-                    const Split& sp, cudaStream_t st) {
+                    const Split& sp, cudaStream_t st, bool complex_factor) {
   if (g_tma_disabled) return -1;
   const bool kc = (nl == 1);
   const int64_t tiles = ((M + tma::BM - 1) / tma::BM) * ((N + tma::BN - 1) / tma::BN);
@@ -64,10 +64,15 @@ int launch_tma_c128(const void* u, const void* L, void* out, int64_t M, int N, i
   if (static_cast<int64_t>(K) * 16 >= (int64_t(1) << 40) || M >= (int64_t(1) << 32)) return -1;
 
   CUtensorMap ma, mb;
-  {  // B: row-major factor, dims (16 f64 = 8 complex k, rows, k groups)
+  if (complex_factor) {  // B: row-major complex factor, dims (16 f64 = 8 complex k, rows, k groups)
     cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(K / 8)};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(K) * 16, 128};
     cuuint32_t box[3] = {16, tma::BN, 2};
+    if (!make_map(&mb, L, 3, dims, strides, box)) return -1;
+  } else {  // real factor: dims (k, rows), 128-B rows of 16 k
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(N), 1};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(K) * 8, static_cast<cuuint64_t>(K) * 8 * N};
+    cuuint32_t box[3] = {16, tma::BN, 1};
     if (!make_map(&mb, L, 3, dims, strides, box)) return -1;
   }
   if (kc) {
@@ -86,11 +91,16 @@ int launch_tma_c128(const void* u, const void* L, void* out, int64_t M, int N, i
     cuuint32_t box[5] = {16, tma::BKS, tma::BM / 8, 1, 1};
     if (!make_map(&ma, u, 5, dims, strides, box)) return -1;
   }
-  if (kc) return launch<true, KM_OP_NONE>(ma, mb, out, M, N, K, nl, op, sp, st);
+  if (!complex_factor) {
+    if (op.kind != KM_OP_NONE) return -1;
+    if (kc) return launch<true, KM_OP_NONE, false>(ma, mb, out, M, N, K, nl, op, sp, st);
+    return launch<false, KM_OP_NONE, false>(ma, mb, out, M, N, K, nl, op, sp, st);
+  }
+  if (kc) return launch<true, KM_OP_NONE, true>(ma, mb, out, M, N, K, nl, op, sp, st);
   switch (op.kind) {
-    case KM_OP_GPE_PHASE: return launch<false, KM_OP_GPE_PHASE>(ma, mb, out, M, N, K, nl, op, sp, st);
-    case KM_OP_DIAG: return launch<false, KM_OP_DIAG>(ma, mb, out, M, N, K, nl, op, sp, st);
-    default: return launch<false, KM_OP_NONE>(ma, mb, out, M, N, K, nl, op, sp, st);
+    case KM_OP_GPE_PHASE: return launch<false, KM_OP_GPE_PHASE, true>(ma, mb, out, M, N, K, nl, op, sp, st);
+    case KM_OP_DIAG: return launch<false, KM_OP_DIAG, true>(ma, mb, out, M, N, K, nl, op, sp, st);
+    default: return launch<false, KM_OP_NONE, true>(ma, mb, out, M, N, K, nl, op, sp, st);
   }
 }
 

@@ -94,7 +94,12 @@ __device__ __forceinline__ void load5(void* dst, const CUtensorMap* m, uint64_t*
 
 }  // namespace tma
 
-template <bool KC, int OPK>
+// CL = false: real factor (e.g. the Hermite Φ), 2 DMMA per complex multiply-add.
+// Its box is (16 real k, 64 rows) in 128-B rows; one LDS.128 fetches the
+// factor values of two consecutive k-steps (k = 2c, 2c+1 share a 16-B chunk
+// under the k permutation above; 2-way bank conflicts on these reads, which the
+// DMMA rate leaves 4x headroom for).
+template <bool KC, int OPK, bool CL = true>
 __global__ void __launch_bounds__(tma::THREADS, 1)
     mumode_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                       double2* __restrict__ out, int64_t M, int N, int K, int64_t nl, const OpDev op,
@@ -131,7 +136,7 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
     const int n0 = static_cast<int>(tile % nN) * BN;
     const int64_t m0 = (tile / nN) * BM;
     unsigned char* st = smem + s * STAGE_BYTES;
-    tma::mbar_expect_tx(&full[s], STAGE_BYTES);
+    tma::mbar_expect_tx(&full[s], CL ? STAGE_BYTES : A_BYTES + BN * BKS * 8);
     const int k0 = kt * BKS;
     if constexpr (KC) {
       tma::load3(st, &mapA, &full[s], 0, static_cast<int>(m0), k0 / 8);
@@ -140,7 +145,10 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
       tma::load5(st, &mapA, &full[s], 0, k0 - kb * sp.kcb, static_cast<int>((m0 % nl) / 8), static_cast<int>(m0 / nl),
                  kb);
     }
-    tma::load3(st + A_BYTES, &mapB, &full[s], 0, n0, k0 / 8);
+    if constexpr (CL)
+      tma::load3(st + A_BYTES, &mapB, &full[s], 0, n0, k0 / 8);
+    else
+      tma::load3(st + A_BYTES, &mapB, &full[s], k0, n0, 0);
   };
   const bool leader = (warp == 0 && lane == 0);
   if (leader) {
@@ -177,29 +185,48 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
       const int s = static_cast<int>(q % TSTAGES);
       tma::mbar_wait(&full[s], static_cast<unsigned>((q / TSTAGES) & 1));
       const unsigned st = sbase + s * STAGE_BYTES;
+      double2 breal[4];
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
         const unsigned ao = ((ks & 1) ? a1 : a0) + (ks >> 1) * A_KG;
-        const unsigned bo = ((ks & 1) ? b1 : b0) + (ks >> 1) * B_KG;
-        double2 a[4], b[4];
+        double2 a[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) a[i] = tma::lds128(st + ao + i * A_I);
+        if constexpr (CL) {
+          const unsigned bo = ((ks & 1) ? b1 : b0) + (ks >> 1) * B_KG;
+          double2 b[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) b[j] = tma::lds128(st + bo + j * B_J);
+          for (int j = 0; j < 4; ++j) b[j] = tma::lds128(st + bo + j * B_J);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
-            dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
+            for (int j = 0; j < 4; ++j) {
+              dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
+              dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
+            }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              dmma(cr[i][j][0], cr[i][j][1], a[i].y, negate(b[j].y));
+              dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
+            }
+        } else {
+          if ((ks & 1) == 0) {
+            // row n = wn + 8j + g holds k = 0..15; chunk (k/2) ^ (n % 8), k/2 = (ks/2)*4 + t
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              breal[j] = tma::lds128(st + A_BYTES + (wn + j * 8 + g) * 128 + ((((ks >> 1) * 4 + t) ^ g) << 4));
           }
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            dmma(cr[i][j][0], cr[i][j][1], a[i].y, negate(b[j].y));
-            dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
-          }
+            for (int j = 0; j < 4; ++j) {
+              const double bv = (ks & 1) ? breal[j].y : breal[j].x;
+              dmma(cr[i][j][0], cr[i][j][1], a[i].x, bv);
+              dmma(ci[i][j][0], ci[i][j][1], a[i].y, bv);
+            }
+        }
       }
       __syncwarp();
       if (lane == 0) tma::mbar_arrive(&empty[s]);
@@ -234,6 +261,6 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
 // Host side: tensor maps + launch.  Returns -1 when the shape is not eligible
 // (the caller then uses the cp.async kernel).
 int launch_tma_c128(const void* u, const void* L, void* out, int64_t M, int N, int K, int64_t nl, const OpDev& op,
-                    const Split& sp, cudaStream_t st);
+                    const Split& sp, cudaStream_t st, bool complex_factor = true);
 
 }  // namespace kmb

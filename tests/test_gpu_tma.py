@@ -76,3 +76,22 @@ def test_tma_blocked_layouts_virtual_ranks(steps):
     for _ in range(steps):
         ref.step()
     assert orc.rel_l2(grp.gather(), dv.to_host(ref.state)) <= 1e-12
+
+
+@pytest.mark.parametrize("shape,mu", [((264, 300, 40), 1), ((128, 200, 104), 2), ((128, 200, 104), 3),
+                                      ((256, 256, 256), 1), ((256, 256, 256), 2), ((256, 256, 256), 3)])
+def test_tma_real_factor_products(shape, mu):
+    """complex tensor x real factor (the Hermite transforms' shape of product)"""
+    import torch
+
+    from paper_2103_01691_b200 import _device as dv
+
+    rng = np.random.default_rng(sum(shape) * 3 + mu)
+    u = crand(rng, shape)
+    n = shape[mu - 1]
+    mat = rng.standard_normal((n + 8, n))  # rectangular: m != n_mu
+    t = dv.to_device(u, np.complex128, torch.device("cuda", 0))
+    a, b = both_policies(lambda: dv.to_host(km.mu_mode_product(t, mat, mu)))
+    want = orc.mu_mode_product(u, mat, mu)
+    assert orc.rel_l2(a, want) <= 1e-13
+    assert orc.rel_l2(b, want) <= 1e-13
