@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define KMB200_ABI_VERSION 1
+#define KMB200_ABI_VERSION 2
 #define KM_MAX_D 8
 
 /* element types; complex values are interleaved (re, im) pairs */
@@ -63,6 +63,12 @@ typedef struct km_pointop {
   const void* diag;                   /* KM_OP_DIAG, c128 vector of dims[diag_dir] */
   int32_t diag_dir;                   /* KM_OP_DIAG, 0-based direction */
   int32_t pad_;
+  /* KM_OP_GPE_PHASE, optional: the weight product over directions 1..d-1,
+   * w_1[i_1]*...*w_{d-1}[i_{d-1}] accumulated left to right, as a column-major
+   * device f64 vector of dims[0]*...*dims[d-2] entries.  With it the kernels
+   * form the full product as inner[l] * w_d[i_d] (same rounding) without
+   * per-element index divisions. */
+  const double* inner_weights;
 } km_pointop;
 
 /* kernel selection (process-wide): AUTO picks the warp-specialised TMA

@@ -15,7 +15,7 @@ import threading
 from .errors import ConfigurationError, DeviceError, NativeLibraryError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libkmb200.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 MAX_D = 8
 
 KM_F32, KM_F64, KM_C64, KM_C128 = 0, 1, 2, 3
@@ -51,6 +51,7 @@ class PointOp(ctypes.Structure):
         ("diag", ctypes.c_void_p),
         ("diag_dir", ctypes.c_int32),
         ("pad_", ctypes.c_int32),
+        ("inner_weights", ctypes.c_void_p),
     ]
 
 

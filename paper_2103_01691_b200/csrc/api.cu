@@ -45,6 +45,10 @@ OpDev to_dev(const km_pointop* op) {
   int64_t s = 1;
   for (int i = 0; i < op->diag_dir && i < op->d; ++i) s *= op->dims[i];
   o.diag_stride = s;
+  o.winner = op->inner_weights;
+  int64_t in = 1;
+  for (int i = 0; i + 1 < op->d; ++i) in *= op->dims[i];
+  o.inner = in;
   return o;
 }
 
@@ -142,12 +146,24 @@ int pointwise_t(const void* in, void* out, int64_t n, const OpDev& op, cudaStrea
   const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
+  dim3 grid(static_cast<unsigned>(blocks));
+  const bool split = (op.kind == KM_OP_GPE_PHASE && op.winner) ||
+                     (op.kind == KM_OP_DIAG && op.diag_dir == op.d - 1);
+  if (split && op.inner > 0 && n % op.inner == 0) {
+    // 2-D grid: x over directions 1..d-1, y over the last direction
+    const int64_t nlast = n / op.inner;
+    int64_t bx = (op.inner + threads - 1) / threads;
+    int64_t by = nlast;
+    if (by > 65535) by = 65535;
+    while (bx * by > cap && bx > 1) bx = (bx + 1) / 2;
+    while (bx * by > cap && by > 1) by = (by + 1) / 2;
+    grid = dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by));
+  }
   if (op.kind == KM_OP_GPE_PHASE)
-    pointwise_kernel<T, KM_OP_GPE_PHASE><<<(unsigned)blocks, threads, 0, st>>>(static_cast<const T*>(in),
-                                                                                static_cast<T*>(out), n, op);
+    pointwise_kernel<T, KM_OP_GPE_PHASE><<<grid, threads, 0, st>>>(static_cast<const T*>(in), static_cast<T*>(out),
+                                                                    n, op);
   else
-    pointwise_kernel<T, KM_OP_DIAG><<<(unsigned)blocks, threads, 0, st>>>(static_cast<const T*>(in),
-                                                                           static_cast<T*>(out), n, op);
+    pointwise_kernel<T, KM_OP_DIAG><<<grid, threads, 0, st>>>(static_cast<const T*>(in), static_cast<T*>(out), n, op);
   return check_launch("pointwise_kernel");
 }
 

@@ -233,6 +233,7 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
     }
 
     // epilogue (overlaps the producer's loads for the next tile)
+    const bool split_op = (OPK != KM_OP_NONE) && !KC && op_split_ok(op, M, nl);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int64_t f = m0 + wm + i * 8 + g;
@@ -250,7 +251,10 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
           if (col >= N) continue;
           const int64_t p = obj + static_cast<int64_t>(col) * cs;
           double re = cr[i][j][h], im = ci[i][j][h];
-          if constexpr (OPK != KM_OP_NONE) apply_op<OPK>(op, p, re, im);
+          if constexpr (OPK != KM_OP_NONE) {
+            if (split_op) apply_op_split<OPK>(op, f, col, re, im);
+            else apply_op<OPK>(op, p, re, im);
+          }
           out[p] = make_double2(re, im);
         }
       }

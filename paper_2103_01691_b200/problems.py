@@ -54,7 +54,17 @@ __all__ = [
 # pointwise operators handed to the C ABI
 
 
-def _gpe_op(shape, weights_dev, half_tau):
+def _inner_weight_product(weights, shape):
+    """w_1 ... w_{d-1} accumulated left to right as problems.py:528-539 does, flattened column-major."""
+    d = len(shape)
+    inner = np.ones(shape[:-1], order="F")
+    for ax, w in enumerate(weights[:-1]):
+        w = w.detach().cpu().numpy() if dv.is_tensor(w) else np.asarray(w, dtype=float)
+        inner *= w.reshape((1,) * ax + (w.size,) + (1,) * (d - 2 - ax))
+    return inner.reshape(-1, order="F")
+
+
+def _gpe_op(shape, weights_dev, half_tau, inner_dev=None):
     op = _native.PointOp()
     op.kind = _native.OP_GPE_PHASE
     op.d = len(shape)
@@ -62,6 +72,8 @@ def _gpe_op(shape, weights_dev, half_tau):
         op.dims[i] = n
         op.weights[i] = weights_dev[i].data_ptr()
     op.coef = 0.5 * half_tau  # the i*0.5*half_tau of problems.py:545
+    if inner_dev is not None:
+        op.inner_weights = inner_dev.data_ptr()
     return op
 
 
@@ -111,9 +123,12 @@ def gpe_strang_step(linear_cache, weights, psi, tau, _timer=None):
     out_dtype = _strang_dtype(po.dtype, linear_cache)
     dev = po.obj.device if po.is_tensor and po.obj.is_cuda else dv.device()
     w_dev = [dv.cached_vector(w, np.float64, dev) for w in weights]
+    inner_dev = dv.cached_vector(_inner_weight_product(weights, po.shape), np.float64, dev) if len(po.shape) > 1 else None
+    if inner_dev is not None:
+        w_dev.append(inner_dev)  # kept alive with the others
     half_tau = 0.5 * tau
-    pre = _gpe_op(po.shape, w_dev, half_tau)
-    post = _gpe_op(po.shape, w_dev, half_tau)
+    pre = _gpe_op(po.shape, w_dev, half_tau, inner_dev)
+    post = _gpe_op(po.shape, w_dev, half_tau, inner_dev)
     state = po.obj
     if po.dtype != out_dtype and not po.is_tensor:
         state = np.asarray(state).astype(out_dtype, order="F")

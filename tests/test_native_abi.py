@@ -41,8 +41,8 @@ def test_library_is_sm100a_cubin():
 
 
 def test_struct_layout_matches_header():
-    # km_pointop: 2*int32 + 8*int64 + 8*ptr + double + ptr + 2*int32
-    assert ctypes.sizeof(_native.PointOp) == 8 + 64 + 64 + 8 + 8 + 8
+    # km_pointop: 2*int32 + 8*int64 + 8*ptr + double + ptr + 2*int32 + ptr
+    assert ctypes.sizeof(_native.PointOp) == 8 + 64 + 64 + 8 + 8 + 8 + 8
 
 
 def test_bad_dtype_rejected_without_device():
