@@ -14,7 +14,8 @@ import threading
 
 from .errors import ConfigurationError, DeviceError, NativeLibraryError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libkmb200.so")
+# KMB200_LIB overrides the library path (A/B builds of the same ABI)
+LIB_PATH = os.environ.get("KMB200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libkmb200.so")
 ABI_VERSION = 2
 MAX_D = 8
 

@@ -61,6 +61,7 @@ int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t 
   if ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(ws)) & 15) return -1;
   if (K % 4 != 0 || m > (1 << 20) || K > (1 << 20)) return -1;
   if (!kc && nl % (tc32::BNR / 2) != 0) return -1;  // a tile's fibers lie inside one slab
+  if ((kc ? 2 * K : K) > 512) return -1;  // accumulation error grows with K' (see kmb200_tc32.cuh)
   if (F >= (int64_t(1) << 31)) return -1;
   float* planes = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
   {

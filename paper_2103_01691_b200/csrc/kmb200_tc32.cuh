@@ -16,7 +16,10 @@
 //     cr = D[2n][2f] - D[2n+1][2f+1], ci = D[2n][2f+1] + D[2n+1][2f] is formed
 //     in the epilogue with one lane shuffle.
 // Both are exactly 4 real multiply-adds per complex multiply-add (x3 for the
-// split).  E's hi/lo planes are prepared once per call (prep_planes_kernel);
+// split).  Accuracy: the tensor core's fp32 accumulation loses ~7e-9 relative
+// per accumulated k (measured: 1.0e-6 / 1.9e-6 / 3.7e-6 rel. l2 at K' = 128 /
+// 256 / 512 against complex128), so the host uses this kernel only up to
+// K' = 512 and keeps longer contractions on the DMMA path (1e-5 bar).  E's hi/lo planes are prepared once per call (prep_planes_kernel);
 // the tensor tile is split in shared memory by four transform warps.
 //
 // Warp roles (10 warps): 0 TMA producer, 1 MMA issuer + TMEM owner,
@@ -94,6 +97,24 @@ __device__ __forceinline__ void ld32(uint32_t taddr, float (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float4 lds_f4(unsigned a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_f4(unsigned a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void sts_f1(unsigned a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;\n" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ float lds_f1(unsigned a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v) : "r"(a) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ float tf32_hi(float x) {
@@ -260,16 +281,36 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
       for (int kt = 0; kt < KT; ++kt, ++q) {
         const int s = static_cast<int>(q % ST);
         tma::mbar_wait(&full[s], static_cast<unsigned>((q / ST) & 1));
-        float4* raw = reinterpret_cast<float4*>(smem + s * STAGE_BYTES + OFF_B);
-        float4* lo = reinterpret_cast<float4*>(smem + s * STAGE_BYTES + OFF_BLO);
+        [[maybe_unused]] const unsigned raw = sbase + s * STAGE_BYTES + OFF_B + tt * 16;
+        const unsigned lo = sbase + s * STAGE_BYTES + OFF_BLO + tt * 16;
+        constexpr int J = PLANE_B / 16 / 128;
+#ifndef KMB_EXP_NO_SPLIT
+        float4 x[J];
 #pragma unroll
-        for (int j = 0; j < PLANE_B / 16 / 128; ++j) {
-          const int idx = tt + 128 * j;
-          float4 x = raw[idx];
-          float4 h = make_float4(tc32::tf32_hi(x.x), tc32::tf32_hi(x.y), tc32::tf32_hi(x.z), tc32::tf32_hi(x.w));
-          raw[idx] = h;
-          lo[idx] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+        for (int j = 0; j < J; ++j) x[j] = tc32::lds_f4(raw + j * 2048);
+#ifndef KMB_EXP_RNA_HI
+        // The tensor core reads an fp32 operand as tf32 by truncating the low 13
+        // mantissa bits (verified: a rounding reader would leave ~5e-4 errors in
+        // tests/test_gpu_tc32.py).  So the raw tile already is "hi" and only
+        // lo = x - trunc(x) (exact in fp32) is written.
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const float4 h = make_float4(__uint_as_float(__float_as_uint(x[j].x) & 0xFFFFE000u),
+                                       __uint_as_float(__float_as_uint(x[j].y) & 0xFFFFE000u),
+                                       __uint_as_float(__float_as_uint(x[j].z) & 0xFFFFE000u),
+                                       __uint_as_float(__float_as_uint(x[j].w) & 0xFFFFE000u));
+          tc32::sts_f4(lo + j * 2048, make_float4(x[j].x - h.x, x[j].y - h.y, x[j].z - h.z, x[j].w - h.w));
         }
+#else
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const float4 h =
+              make_float4(tc32::tf32_hi(x[j].x), tc32::tf32_hi(x[j].y), tc32::tf32_hi(x[j].z), tc32::tf32_hi(x[j].w));
+          tc32::sts_f4(raw + j * 2048, h);
+          tc32::sts_f4(lo + j * 2048, make_float4(x[j].x - h.x, x[j].y - h.y, x[j].z - h.z, x[j].w - h.w));
+        }
+#endif
+#endif
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) tma::mbar_arrive(&ready[s]);
@@ -298,19 +339,21 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int64_t f = c0 + ch * 32 + j;
+#ifndef KMB_EXP_NO_STORE
             if (n < m && f < F) outf[2 * (f * m + n) + part] = v[j];
+#endif
           }
         } else {
           // columns 2f+c; cr = D[2n][2f] - D[2n+1][2f+1], ci = D[2n][2f+1] + D[2n+1][2f].
           // Lane 2n'+part ends up with 16 fibers of output row n'; a transpose through
           // shared memory gives lane 2f+part the 16 rows of fiber f, so every store
           // instruction writes 128 contiguous bytes (16 fibers x complex64 of one row).
-          float* xb = xbuf_all + (warp - 6) * (XBUF / 4);
+          const unsigned xb = tma::su32(xbuf_all) + (warp - 6) * XBUF;
           const int np = lane >> 1;
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const float x = __shfl_xor_sync(0xffffffffu, v[2 * j + 1], 1);
-            xb[np * XPITCH + 2 * j + part] = part ? v[2 * j] + x : v[2 * j] - x;
+            tc32::sts_f1(xb + (np * XPITCH + 2 * j + part) * 4, part ? v[2 * j] + x : v[2 * j] - x);
           }
           __syncwarp();
           // the tile's fibers lie inside one n_left slab: one division per tile
@@ -321,7 +364,10 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int nn = nbase + j;
-            if (fok && nn < m) outf[2 * (fl + r * nl * m + static_cast<int64_t>(nn) * nl) + part] = xb[j * XPITCH + lane];
+            const float val = tc32::lds_f1(xb + (j * XPITCH + lane) * 4);
+#ifndef KMB_EXP_NO_STORE
+            if (fok && nn < m) outf[2 * (fl + r * nl * m + static_cast<int64_t>(nn) * nl) + part] = val;
+#endif
           }
           __syncwarp();
         }

@@ -52,3 +52,13 @@ def test_c64_step_256_vs_oracle_and_dmma():
     finally:
         _native.check(lib.km_set_kernel_policy(_native.POLICY_AUTO))
     assert orc.rel_l2(got, dmma) <= 1e-5
+
+
+def test_long_contraction_stays_on_dmma_and_accurate():
+    # K' = 2*n_mu > 512 for direction 1: the host keeps it on the DMMA path
+    rng = np.random.default_rng(9)
+    u = crand(rng, (384, 64, 8))
+    mat = ((rng.standard_normal((384, 384)) + 1j * rng.standard_normal((384, 384))) / 20).astype(np.complex64)
+    got = km.mu_mode_product(u, mat, 1)
+    want128 = orc.mu_mode_product(u.astype(np.complex128), mat.astype(np.complex128), 1)
+    assert orc.rel_l2(got, want128) <= 1e-6
