@@ -32,8 +32,8 @@ bool map_f32(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
 }
 
 template <bool KC>
-int launch(const CUtensorMap& ahi, const CUtensorMap& alo, const CUtensorMap& b, void* out, int64_t F, int m, int K,
-           int64_t nl, cudaStream_t st) {
+int launch(const CUtensorMap& ahi, const CUtensorMap& alo, const CUtensorMap& b, const CUtensorMap& mo, int64_t F,
+           int m, int K, int64_t nl, cudaStream_t st) {
   auto kern = mumode_tc32_kernel<KC>;
   static bool attr = false;
   if (!attr) {
@@ -44,7 +44,7 @@ int launch(const CUtensorMap& ahi, const CUtensorMap& alo, const CUtensorMap& b,
   const int64_t fib_r = KC ? F : 2 * F;
   const int64_t tiles = ((2 * m + tc32::BMR - 1) / tc32::BMR) * ((fib_r + tc32::BNR - 1) / tc32::BNR);
   const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
-  kern<<<grid, tc32::THREADS, tc32::SMEM_BYTES, st>>>(ahi, alo, b, static_cast<float2*>(out), F, m, K, nl);
+  kern<<<grid, tc32::THREADS, tc32::SMEM_BYTES, st>>>(ahi, alo, b, mo, F, m, K, nl);
   return check_launch("mumode_tc32_kernel");
 }
 
@@ -59,7 +59,8 @@ int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t 
   const int64_t F = nl * nr;
   if (!ws || ws_bytes < tc32_workspace_bytes(m, K)) return -1;
   if ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(ws)) & 15) return -1;
-  if (K % 4 != 0 || m > (1 << 20) || K > (1 << 20)) return -1;
+  if (K % 4 != 0 || m % 2 != 0 || m > (1 << 20) || K > (1 << 20)) return -1;
+  if (reinterpret_cast<uintptr_t>(out) & 15) return -1;
   if (!kc && nl % (tc32::BNR / 2) != 0) return -1;  // a tile's fibers lie inside one slab
   if ((kc ? 2 * K : K) > 512) return -1;  // accumulation error grows with K' (see kmb200_tc32.cuh)
   if (F >= (int64_t(1) << 31)) return -1;
@@ -91,7 +92,13 @@ int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t 
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(2 * K) * 4, static_cast<cuuint64_t>(2 * K) * 4 * F};
     cuuint32_t box[3] = {tc32::BKR, tc32::BNR, 1};
     if (!map_f32(&mb, u, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B)) return -1;
-    return launch<true>(mahi, malo, mb, out, F, static_cast<int>(m), static_cast<int>(K), nl, st);
+    // output (F x m complex, row-major in n): boxes of 32 fibers x 16 complex n
+    CUtensorMap mo;
+    cuuint64_t od[3] = {static_cast<cuuint64_t>(2 * m), static_cast<cuuint64_t>(F), 1};
+    cuuint64_t os[2] = {static_cast<cuuint64_t>(2 * m) * 4, static_cast<cuuint64_t>(2 * m) * 4 * F};
+    cuuint32_t ob[3] = {32, 32, 1};
+    if (!map_f32(&mo, out, 3, od, os, ob)) return -1;
+    return launch<true>(mahi, malo, mb, mo, F, static_cast<int>(m), static_cast<int>(K), nl, st);
   }
   cuuint64_t dims[5] = {32, static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(nl / 16), static_cast<cuuint64_t>(nr),
                         1};
@@ -100,7 +107,13 @@ int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t 
   cuuint32_t box[5] = {32, tc32::BKR, tc32::BNR / 32, 1, 1};
   // MN-major tf32 operand: 32-B swizzle atoms (matches the BASE32B descriptor layout)
   if (!map_f32(&mb, u, 5, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return -1;
-  return launch<false>(mahi, malo, mb, out, F, static_cast<int>(m), static_cast<int>(K), nl, st);
+  // output (n_left x m x n_right complex): boxes of 16 fibers x 16 rows n
+  CUtensorMap mo;
+  cuuint64_t od[3] = {static_cast<cuuint64_t>(2 * nl), static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(nr)};
+  cuuint64_t os[2] = {static_cast<cuuint64_t>(nl) * 8, static_cast<cuuint64_t>(nl) * m * 8};
+  cuuint32_t ob[3] = {32, 16, 1};
+  if (!map_f32(&mo, out, 3, od, os, ob)) return -1;
+  return launch<false>(mahi, malo, mb, mo, F, static_cast<int>(m), static_cast<int>(K), nl, st);
 }
 
 }  // namespace kmb

@@ -43,9 +43,8 @@ constexpr int OFF_ALO = PLANE_A, OFF_B = 2 * PLANE_A, OFF_BLO = 2 * PLANE_A + PL
 constexpr int STAGE_BYTES = 2 * PLANE_A + 2 * PLANE_B;
 constexpr int TX_BYTES = 2 * PLANE_A + PLANE_B;  // bytes TMA lands per stage
 constexpr int THREADS = 320;
-constexpr int XPITCH = 34;  // epilogue transpose buffer row pitch (floats): conflict-free both ways
-constexpr int XBUF = 16 * XPITCH * 4;  // per epilogue warp
-constexpr int SMEM_BYTES = ST * STAGE_BYTES + 4 * XBUF + 1024 + 256;
+constexpr int XSTAGE = 32 * 128;  // per epilogue warp: one 32 x 32-float (KC) or 16 x 32 (MC) output box
+constexpr int SMEM_BYTES = ST * STAGE_BYTES + 1024 + 4 * XSTAGE + 1024;
 constexpr int TMEM_COLS = 512;  // two 256-column accumulators
 
 // layout: 4 = SWIZZLE_64B (K-major operands, 64-B rows), 1 = SWIZZLE_128B_BASE32B
@@ -117,6 +116,15 @@ __device__ __forceinline__ float lds_f1(unsigned a) {
   return v;
 }
 
+__device__ __forceinline__ void store3(const CUtensorMap* m, unsigned src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];\n" ::"l"(m),
+               "r"(src), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
 __device__ __forceinline__ float tf32_hi(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
@@ -160,7 +168,8 @@ __global__ void prep_planes_kernel(const float2* __restrict__ L, float* __restri
 template <bool KC>
 __global__ void __launch_bounds__(tc32::THREADS, 1)
     mumode_tc32_kernel(const __grid_constant__ CUtensorMap mapAhi, const __grid_constant__ CUtensorMap mapAlo,
-                       const __grid_constant__ CUtensorMap mapB, float2* __restrict__ out, int64_t F, int m, int K,
+                       const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapOut, int64_t F,
+                       int m, int K,
                        int64_t nl) {
   using namespace tc32;
   extern __shared__ unsigned char smem_raw[];
@@ -172,7 +181,7 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
   uint64_t* tfull = empty + ST;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* xbuf_all = reinterpret_cast<float*>(smem + ST * STAGE_BYTES + 256);
+  unsigned char* xstage = smem + ST * STAGE_BYTES + 1024;  // 1024-B aligned (128-B swizzle)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -318,8 +327,11 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
+    // TMEM -> registers -> swizzled shared staging (4 KB per warp) -> TMA store.
+    // The staging layout is the output box with the 128-B swizzle, so the
+    // staging writes are bank-conflict free (KC) or 2-way (MC).
     const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
-    const int row = quarter * 32 + lane;
+    const unsigned stg = tma::su32(xstage) + (warp - 6) * XSTAGE;
     for (int64_t it = 0; it < my_tiles; ++it) {
       const int64_t tile = blockIdx.x + it * gridDim.x;
       const int e0 = static_cast<int>(tile % nE) * BMR;
@@ -327,55 +339,46 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
       const int b = static_cast<int>(it & 1);
       tma::mbar_wait(&tfull[b], static_cast<unsigned>((it >> 1) & 1));
       fence_after();
-      const int er = e0 + row;  // real row of E: n = er / 2, part = er & 1
-      const int n = er >> 1, part = er & 1;
-      float* outf = reinterpret_cast<float*>(out);
+      const int nbase = (e0 >> 1) + quarter * 16;  // first output row (complex) of this warp
 #pragma unroll 1
       for (int ch = 0; ch < BNR / 32; ++ch) {
         float v[32];
         ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + b * BNR + ch * 32, v);
+        if (lane == 0) tc32::bulk_wait_read();  // the previous store from this staging buffer has read it
+        __syncwarp();
         if constexpr (KC) {
-          // D[2n+part][f] = part ? ci : cr of output (f, n); out[f*m + n]
+          // D[2n+part][f]: lane = 2n'+part = the float column of the (f, 16 complex n) box
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int64_t f = c0 + ch * 32 + j;
-#ifndef KMB_EXP_NO_STORE
-            if (n < m && f < F) outf[2 * (f * m + n) + part] = v[j];
-#endif
-          }
+          for (int j = 0; j < 32; ++j)
+            tc32::sts_f1(stg + j * 128 + ((((lane >> 2) ^ (j & 7))) << 4) + (lane & 3) * 4, v[j]);
         } else {
-          // columns 2f+c; cr = D[2n][2f] - D[2n+1][2f+1], ci = D[2n][2f+1] + D[2n+1][2f].
-          // Lane 2n'+part ends up with 16 fibers of output row n'; a transpose through
-          // shared memory gives lane 2f+part the 16 rows of fiber f, so every store
-          // instruction writes 128 contiguous bytes (16 fibers x complex64 of one row).
-          const unsigned xb = tma::su32(xbuf_all) + (warp - 6) * XBUF;
-          const int np = lane >> 1;
+          // columns 2f+c; cr = D[2n][2f] - D[2n+1][2f+1], ci = D[2n][2f+1] + D[2n+1][2f]
+          const int np = lane >> 1, part = lane & 1;
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const float x = __shfl_xor_sync(0xffffffffu, v[2 * j + 1], 1);
-            tc32::sts_f1(xb + (np * XPITCH + 2 * j + part) * 4, part ? v[2 * j] + x : v[2 * j] - x);
+            const int c = 2 * j + part;
+            tc32::sts_f1(stg + np * 128 + ((((c >> 2) ^ (np & 7))) << 4) + (c & 3) * 4,
+                         part ? v[2 * j] + x : v[2 * j] - x);
           }
-          __syncwarp();
-          // the tile's fibers lie inside one n_left slab: one division per tile
-          const int64_t ft = c0 / 2 + ch * 16, r = ft / nl;
-          const int64_t fl = ft - r * nl + (lane >> 1);
-          const int nbase = (e0 >> 1) + quarter * 16;
-          const bool fok = ft + (lane >> 1) < F;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int nn = nbase + j;
-            const float val = tc32::lds_f1(xb + (j * XPITCH + lane) * 4);
-#ifndef KMB_EXP_NO_STORE
-            if (fok && nn < m) outf[2 * (fl + r * nl * m + static_cast<int64_t>(nn) * nl) + part] = val;
-#endif
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (KC) {
+            tc32::store3(&mapOut, stg, 2 * nbase, static_cast<int>(c0 + ch * 32), 0);
+          } else {
+            const int64_t ft = c0 / 2 + ch * 16, r = ft / nl;  // the tile lies inside one n_left slab
+            tc32::store3(&mapOut, stg, static_cast<int>(2 * (ft - r * nl)), nbase, static_cast<int>(r));
           }
-          __syncwarp();
+          tc32::bulk_commit();
         }
       }
       fence_before();
       __syncwarp();
       if (lane == 0) tma::mbar_arrive(&tempty[b]);
     }
+    if (lane == 0) tc32::bulk_wait_all();
   }
   fence_before();
   __syncthreads();
