@@ -32,10 +32,10 @@ bool make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims
   return r == CUDA_SUCCESS;
 }
 
-template <bool KC, int OPK, bool CL>
+template <bool KC, int OPK, bool CL, bool CU>
 int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* out, int64_t M, int N, int K, int64_t nl,
            const OpDev& op, const Split& sp, cudaStream_t st) {
-  auto kern = mumode_tma_kernel<KC, OPK, CL>;
+  auto kern = mumode_tma_kernel<KC, OPK, CL, CU>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tma::SMEM_BYTES);
@@ -44,7 +44,8 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* out, int64_t M, i
   }
   const int64_t tiles = ((M + tma::BM - 1) / tma::BM) * ((N + tma::BN - 1) / tma::BN);
   const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
-  kern<<<grid, tma::THREADS, tma::SMEM_BYTES, st>>>(ma, mb, static_cast<double2*>(out), M, N, K, nl, op, sp);
+  kern<<<grid, tma::THREADS, tma::SMEM_BYTES, st>>>(ma, mb, static_cast<typename El<double, CU || CL>::T*>(out), M,
+                                                    N, K, nl, op, sp);
   return check_launch("mumode_tma_kernel");
 }
 
@@ -52,15 +53,16 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* out, int64_t M, i
 
 bool g_tma_disabled = false;
 
-int launch_tma_c128(const void* u, const void* L, void* out, int64_t M, int N, int K, int64_t nl, const OpDev& op,
-                    const Split& sp, cudaStream_t st, bool complex_factor) {
+int launch_tma_f64(const void* u, const void* L, void* out, int64_t M, int N, int K, int64_t nl, const OpDev& op,
+                   const Split& sp, cudaStream_t st, bool complex_tensor, bool complex_factor) {
   if (g_tma_disabled) return -1;
   const bool kc = (nl == 1);
   const int64_t tiles = ((M + tma::BM - 1) / tma::BM) * ((N + tma::BN - 1) / tma::BN);
-  if (K % 8 != 0 || tiles < 2 * num_sms()) return -1;
+  // persistent: worth it once the tiles cover ~3/4 of the SMs (smaller problems use
+  // the cp.async kernel's 4x finer tiles)
+  if (K % 8 != 0 || 4 * tiles < 3 * num_sms()) return -1;
   if ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(L)) & 15) return -1;
   if (!kc && (nl % tma::BM != 0 || (sp.kcb != K && sp.kcb % tma::BKS != 0))) return -1;
-  if (op.kind != KM_OP_NONE && kc) return -1;  // fused ops only in the strided layout
   if (static_cast<int64_t>(K) * 16 >= (int64_t(1) << 40) || M >= (int64_t(1) << 32)) return -1;
 
   CUtensorMap ma, mb;
@@ -75,7 +77,13 @@ int launch_tma_c128(const void* u, const void* L, void* out, int64_t M, int N, i
     cuuint32_t box[3] = {16, tma::BN, 1};
     if (!make_map(&mb, L, 3, dims, strides, box)) return -1;
   }
-  if (kc) {
+  if (kc && !complex_tensor) {  // real, k-contiguous: dims (k, fibers), 128-B rows of 16 k
+    if (K % 2 != 0) return -1;
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M), 1};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(K) * 8, static_cast<cuuint64_t>(K) * 8 * M};
+    cuuint32_t box[3] = {16, tma::BM, 1};
+    if (!make_map(&ma, u, 3, dims, strides, box)) return -1;
+  } else if (kc) {  // complex, k-contiguous: dims (16 f64 = 8 complex k, fibers, k groups)
     cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(K / 8)};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(K) * 16, 128};
     cuuint32_t box[3] = {16, tma::BM, 2};
@@ -83,24 +91,36 @@ int launch_tma_c128(const void* u, const void* L, void* out, int64_t M, int N, i
   } else {
     const int64_t nr = M / nl;
     const int64_t nblk = (K + sp.kcb - 1) / sp.kcb;
+    const int64_t es = complex_tensor ? 16 : 8;  // element bytes
     const int64_t kbs = nblk > 1 ? sp.kbs : static_cast<int64_t>(nl) * sp.kcb * nr;
-    cuuint64_t dims[5] = {16, static_cast<cuuint64_t>(sp.kcb), static_cast<cuuint64_t>(nl / 8),
+    // (one 128-B row of fibers, k in block, fiber rows, n_right, k blocks)
+    const cuuint64_t fib_per_row = 128 / es;
+    cuuint64_t dims[5] = {16, static_cast<cuuint64_t>(sp.kcb), static_cast<cuuint64_t>(nl / fib_per_row),
                           static_cast<cuuint64_t>(nr), static_cast<cuuint64_t>(nblk)};
-    cuuint64_t strides[4] = {static_cast<cuuint64_t>(nl) * 16, 128, static_cast<cuuint64_t>(nl) * sp.kcb * 16,
-                             static_cast<cuuint64_t>(kbs) * 16};
-    cuuint32_t box[5] = {16, tma::BKS, tma::BM / 8, 1, 1};
+    cuuint64_t strides[4] = {static_cast<cuuint64_t>(nl * es), 128, static_cast<cuuint64_t>(nl * sp.kcb * es),
+                             static_cast<cuuint64_t>(kbs * es)};
+    cuuint32_t box[5] = {16, tma::BKS, static_cast<cuuint32_t>(tma::BM / fib_per_row), 1, 1};
     if (!make_map(&ma, u, 5, dims, strides, box)) return -1;
   }
-  if (!complex_factor) {
-    if (op.kind != KM_OP_NONE) return -1;
-    if (kc) return launch<true, KM_OP_NONE, false>(ma, mb, out, M, N, K, nl, op, sp, st);
-    return launch<false, KM_OP_NONE, false>(ma, mb, out, M, N, K, nl, op, sp, st);
+  const bool ops = op.kind != KM_OP_NONE;
+  if (ops && (kc || !(complex_tensor && complex_factor))) return -1;  // fused ops: c x c, strided layout only
+  if (!complex_tensor) {
+    if (complex_factor) {
+      if (kc) return launch<true, KM_OP_NONE, true, false>(ma, mb, out, M, N, K, nl, op, sp, st);
+      return launch<false, KM_OP_NONE, true, false>(ma, mb, out, M, N, K, nl, op, sp, st);
+    }
+    if (kc) return launch<true, KM_OP_NONE, false, false>(ma, mb, out, M, N, K, nl, op, sp, st);
+    return launch<false, KM_OP_NONE, false, false>(ma, mb, out, M, N, K, nl, op, sp, st);
   }
-  if (kc) return launch<true, KM_OP_NONE, true>(ma, mb, out, M, N, K, nl, op, sp, st);
+  if (!complex_factor) {
+    if (kc) return launch<true, KM_OP_NONE, false, true>(ma, mb, out, M, N, K, nl, op, sp, st);
+    return launch<false, KM_OP_NONE, false, true>(ma, mb, out, M, N, K, nl, op, sp, st);
+  }
+  if (kc) return launch<true, KM_OP_NONE, true, true>(ma, mb, out, M, N, K, nl, op, sp, st);
   switch (op.kind) {
-    case KM_OP_GPE_PHASE: return launch<false, KM_OP_GPE_PHASE, true>(ma, mb, out, M, N, K, nl, op, sp, st);
-    case KM_OP_DIAG: return launch<false, KM_OP_DIAG, true>(ma, mb, out, M, N, K, nl, op, sp, st);
-    default: return launch<false, KM_OP_NONE, true>(ma, mb, out, M, N, K, nl, op, sp, st);
+    case KM_OP_GPE_PHASE: return launch<false, KM_OP_GPE_PHASE, true, true>(ma, mb, out, M, N, K, nl, op, sp, st);
+    case KM_OP_DIAG: return launch<false, KM_OP_DIAG, true, true>(ma, mb, out, M, N, K, nl, op, sp, st);
+    default: return launch<false, KM_OP_NONE, true, true>(ma, mb, out, M, N, K, nl, op, sp, st);
   }
 }
 

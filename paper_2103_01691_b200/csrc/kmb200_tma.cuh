@@ -72,6 +72,11 @@ __device__ __forceinline__ double2 lds128(unsigned addr) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ double lds64(unsigned addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(m) : "memory");
@@ -99,11 +104,15 @@ __device__ __forceinline__ void load5(void* dst, const CUtensorMap* m, uint64_t*
 // factor values of two consecutive k-steps (k = 2c, 2c+1 share a 16-B chunk
 // under the k permutation above; 2-way bank conflicts on these reads, which the
 // DMMA rate leaves 4x headroom for).
-template <bool KC, int OPK, bool CL = true>
+// CU = false: real tensor (e.g. the f64 pipe-flow state).  Fiber-contiguous
+// boxes are (16 fibers, 16 k, 8 fiber groups) in 128-B rows and read with one
+// conflict-free LDS.64 per MMA tile; k-contiguous boxes are (16 k, 128 fibers)
+// and read in k pairs with LDS.128 like the real factor.
+template <bool KC, int OPK, bool CL = true, bool CU = true>
 __global__ void __launch_bounds__(tma::THREADS, 1)
     mumode_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                      double2* __restrict__ out, int64_t M, int N, int K, int64_t nl, const OpDev op,
-                      const Split sp) {
+                      typename El<double, CU || CL>::T* __restrict__ out, int64_t M, int N, int K, int64_t nl,
+                      const OpDev op, const Split sp) {
   using namespace tma;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
@@ -136,9 +145,15 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
     const int n0 = static_cast<int>(tile % nN) * BN;
     const int64_t m0 = (tile / nN) * BM;
     unsigned char* st = smem + s * STAGE_BYTES;
-    tma::mbar_expect_tx(&full[s], CL ? STAGE_BYTES : A_BYTES + BN * BKS * 8);
+    tma::mbar_expect_tx(&full[s], (CU ? A_BYTES : A_BYTES / 2) + (CL ? B_BYTES : B_BYTES / 2));
     const int k0 = kt * BKS;
-    if constexpr (KC) {
+    if constexpr (KC && !CU) {
+      tma::load3(st, &mapA, &full[s], k0, static_cast<int>(m0), 0);
+    } else if constexpr (!CU) {
+      const int kb = k0 / sp.kcb;
+      tma::load5(st, &mapA, &full[s], 0, k0 - kb * sp.kcb, static_cast<int>((m0 % nl) / 16), static_cast<int>(m0 / nl),
+                 kb);
+    } else if constexpr (KC) {
       tma::load3(st, &mapA, &full[s], 0, static_cast<int>(m0), k0 / 8);
     } else {
       const int kb = k0 / sp.kcb;
@@ -185,32 +200,61 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
       const int s = static_cast<int>(q % TSTAGES);
       tma::mbar_wait(&full[s], static_cast<unsigned>((q / TSTAGES) & 1));
       const unsigned st = sbase + s * STAGE_BYTES;
-      double2 breal[4];
+      double2 breal[4], areal[4];
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
-        const unsigned ao = ((ks & 1) ? a1 : a0) + (ks >> 1) * A_KG;
         double2 a[4];
+        if constexpr (CU) {
+          const unsigned ao = ((ks & 1) ? a1 : a0) + (ks >> 1) * A_KG;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = tma::lds128(st + ao + i * A_I);
+          for (int i = 0; i < 4; ++i) a[i] = tma::lds128(st + ao + i * A_I);
+        } else if constexpr (KC) {
+          // real, k-contiguous: row f = wm + 8i + g holds k 0..15; one LDS.128 per k pair
+          if ((ks & 1) == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              areal[i] = tma::lds128(st + (wm + i * 8 + g) * 128 + ((((ks >> 1) * 4 + t) ^ g) << 4));
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) a[i] = make_double2((ks & 1) ? areal[i].y : areal[i].x, 0.0);
+        } else {
+          // real, fiber-contiguous: [fiber group][k][16 fibers]; fiber c = 8*(i%2) + g of group wm/16 + i/2
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const unsigned row = (wm / 16 + (i >> 1)) * 16 + (ks >> 1) * 8 + 2 * t + (ks & 1);
+            const unsigned chunk = ((i & 1) * 4 + (g >> 1)) ^ (2 * t + (ks & 1));
+            a[i] = make_double2(tma::lds64(st + row * 128 + (chunk << 4) + (g & 1) * 8), 0.0);
+          }
+        }
         if constexpr (CL) {
           const unsigned bo = ((ks & 1) ? b1 : b0) + (ks >> 1) * B_KG;
           double2 b[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) b[j] = tma::lds128(st + bo + j * B_J);
+          if constexpr (CU) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
-              dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
-            }
+              for (int j = 0; j < 4; ++j) {
+                dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
+                dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
+              }
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              dmma(cr[i][j][0], cr[i][j][1], a[i].y, negate(b[j].y));
-              dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
-            }
+              for (int j = 0; j < 4; ++j) {
+                dmma(cr[i][j][0], cr[i][j][1], a[i].y, negate(b[j].y));
+                dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
+              }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
+                dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
+              }
+          }
         } else {
           if ((ks & 1) == 0) {
             // row n = wn + 8j + g holds k = 0..15; chunk (k/2) ^ (n % 8), k/2 = (ks/2)*4 + t
@@ -224,7 +268,7 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
             for (int j = 0; j < 4; ++j) {
               const double bv = (ks & 1) ? breal[j].y : breal[j].x;
               dmma(cr[i][j][0], cr[i][j][1], a[i].x, bv);
-              dmma(ci[i][j][0], ci[i][j][1], a[i].y, bv);
+              if constexpr (CU) dmma(ci[i][j][0], ci[i][j][1], a[i].y, bv);
             }
         }
       }
@@ -250,12 +294,12 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
           const int col = c8 + 2 * t + h;
           if (col >= N) continue;
           const int64_t p = obj + static_cast<int64_t>(col) * cs;
-          double re = cr[i][j][h], im = ci[i][j][h];
-          if constexpr (OPK != KM_OP_NONE) {
+          double re = cr[i][j][h], im = (CU || CL) ? ci[i][j][h] : 0.0;
+          if constexpr (OPK != KM_OP_NONE && (CU || CL)) {
             if (split_op) apply_op_split<OPK>(op, f, col, re, im);
             else apply_op<OPK>(op, p, re, im);
           }
-          out[p] = make_double2(re, im);
+          out[p] = narrow<typename El<double, CU || CL>::T>(re, im);
         }
       }
     }
@@ -264,7 +308,7 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
 
 // Host side: tensor maps + launch.  Returns -1 when the shape is not eligible
 // (the caller then uses the cp.async kernel).
-int launch_tma_c128(const void* u, const void* L, void* out, int64_t M, int N, int K, int64_t nl, const OpDev& op,
-                    const Split& sp, cudaStream_t st, bool complex_factor = true);
+int launch_tma_f64(const void* u, const void* L, void* out, int64_t M, int N, int K, int64_t nl, const OpDev& op,
+                   const Split& sp, cudaStream_t st, bool complex_tensor, bool complex_factor);
 
 }  // namespace kmb

@@ -95,3 +95,26 @@ def test_tma_real_factor_products(shape, mu):
     want = orc.mu_mode_product(u, mat, mu)
     assert orc.rel_l2(a, want) <= 1e-13
     assert orc.rel_l2(b, want) <= 1e-13
+
+
+@pytest.mark.parametrize("shape,mu,cl", [((1024, 1024), 1, False), ((1024, 1024), 2, False),
+                                         ((264, 300, 40), 1, True), ((256, 256, 256), 2, True),
+                                         ((256, 256, 256), 3, False), ((128, 200, 104), 3, False)])
+def test_tma_real_tensor_products(shape, mu, cl):
+    """real tensor x real factor (pipe flow) and real tensor x complex factor"""
+    import torch
+
+    from paper_2103_01691_b200 import _device as dv
+
+    rng = np.random.default_rng(sum(shape) * 5 + mu)
+    u = np.asfortranarray(rng.standard_normal(shape))
+    n = shape[mu - 1]
+    mat = rng.standard_normal((n, n))
+    if cl:
+        mat = mat + 1j * rng.standard_normal((n, n))
+    t = dv.to_device(u, np.float64, torch.device("cuda", 0))
+    a, b = both_policies(lambda: dv.to_host(km.mu_mode_product(t, mat, mu)))
+    want = orc.mu_mode_product(u, mat, mu)
+    assert a.dtype == want.dtype
+    assert orc.rel_l2(a, want) <= 1e-13
+    assert orc.rel_l2(b, want) <= 1e-13
