@@ -6,15 +6,15 @@
 
 namespace kmb {
 
-template <typename S, bool CU, bool CL, bool KC, int OPK, int WM_, int WN_>
+template <typename S, bool CU, bool CL, bool KC, int OPK, int WM_, int WN_, int WT_ = WT>
 int launch_cfg(const void* u, const void* L, void* out, int64_t M, int N, int K, int64_t nl, const OpDev& op,
                const Split& sp, cudaStream_t st) {
   using TU = typename El<S, CU>::T;
   using TL = typename El<S, CL>::T;
   using TO = typename El<S, CU || CL>::T;
-  constexpr int BM = WT * WM_, BN = WT * WN_;
+  constexpr int BM = WT_ * WM_, BN = WT_ * WN_;
   using Lay = SmemLayout<TU, TL, KC, BM, BN>;
-  auto kern = mumode_kernel<S, CU, CL, KC, OPK, WM_, WN_>;
+  auto kern = mumode_kernel<S, CU, CL, KC, OPK, WM_, WN_, WT_>;
   static bool attr_set = false;  // once per instantiation and process
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL);
@@ -35,6 +35,9 @@ int launch_sized(const void* u, const void* L, void* out, int64_t M, int N, int 
                  const Split& sp, cudaStream_t st) {
   const int64_t big = ((M + 127) / 128) * ((N + 63) / 64);
   if (big >= 2 * num_sms()) return launch_cfg<S, CU, CL, KC, OPK, 4, 2>(u, L, out, M, N, K, nl, op, sp, st);
+  // small tensors: 32x32 tiles of four 16x16 warp tiles, ~4x the warps of the 64x32 variant
+  const int64_t small = ((M + 31) / 32) * ((N + 31) / 32);
+  if (small <= 16 * num_sms()) return launch_cfg<S, CU, CL, KC, OPK, 2, 2, 16>(u, L, out, M, N, K, nl, op, sp, st);
   return launch_cfg<S, CU, CL, KC, OPK, 2, 1>(u, L, out, M, N, K, nl, op, sp, st);
 }
 
