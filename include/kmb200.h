@@ -62,7 +62,8 @@ typedef struct km_pointop {
   double coef;                        /* KM_OP_GPE_PHASE */
   const void* diag;                   /* KM_OP_DIAG, c128 vector of dims[diag_dir] */
   int32_t diag_dir;                   /* KM_OP_DIAG, 0-based direction */
-  int32_t pad_;
+  int32_t repeat;                     /* KM_OP_GPE_PHASE: apply 1 (0 = 1) or 2 times in a row,
+                                         e.g. step k's closing and step k+1's opening half-phase */
   /* KM_OP_GPE_PHASE, optional: the weight product over directions 1..d-1,
    * w_1[i_1]*...*w_{d-1}[i_{d-1}] accumulated left to right, as a column-major
    * device f64 vector of dims[0]*...*dims[d-2] entries.  With it the kernels

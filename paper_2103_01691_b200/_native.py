@@ -51,7 +51,7 @@ class PointOp(ctypes.Structure):
         ("coef", ctypes.c_double),
         ("diag", ctypes.c_void_p),
         ("diag_dir", ctypes.c_int32),
-        ("pad_", ctypes.c_int32),
+        ("repeat", ctypes.c_int32),
         ("inner_weights", ctypes.c_void_p),
     ]
 

@@ -46,6 +46,7 @@ OpDev to_dev(const km_pointop* op) {
   for (int i = 0; i < op->diag_dir && i < op->d; ++i) s *= op->dims[i];
   o.diag_stride = s;
   o.winner = op->inner_weights;
+  o.repeat = op->repeat > 1 ? 2 : 1;
   int64_t in = 1;
   for (int i = 0; i + 1 < op->d; ++i) in *= op->dims[i];
   o.inner = in;
@@ -56,6 +57,7 @@ int validate_op(const km_pointop* op, const char* where) {
   if (!op || op->kind == KM_OP_NONE) return KM_OK;
   if (op->d < 1 || op->d > KM_MAX_D) return fail(KM_EINVAL, "%s: op order %d outside 1..%d", where, op->d, KM_MAX_D);
   if (op->kind == KM_OP_GPE_PHASE) {
+    if (op->repeat < 0 || op->repeat > 2) return fail(KM_EINVAL, "%s: GPE phase repeat %d outside 0..2", where, op->repeat);
     for (int i = 0; i < op->d; ++i)
       if (!op->weights[i]) return fail(KM_EINVAL, "%s: GPE phase weight %d is NULL", where, i);
     return KM_OK;

@@ -38,6 +38,7 @@ from .tensor import _Operand, run_tucker
 __all__ = [
     "VortexProfile",
     "gpe_setup",
+    "gpe_strang_run",
     "gpe_strang_step",
     "hkmp_factors",
     "magnus_midpoint_step",
@@ -64,8 +65,9 @@ def _inner_weight_product(weights, shape):
     return inner.reshape(-1, order="F")
 
 
-def _gpe_op(shape, weights_dev, half_tau, inner_dev=None):
+def _gpe_op(shape, weights_dev, half_tau, inner_dev=None, repeat=1):
     op = _native.PointOp()
+    op.repeat = repeat
     op.kind = _native.OP_GPE_PHASE
     op.d = len(shape)
     for i, n in enumerate(shape):
@@ -139,6 +141,43 @@ def gpe_strang_step(linear_cache, weights, psi, tau, _timer=None):
         with _timer.mode_products():
             return run_tucker(state, mats, pre=pre, post=post, out_dtype=out_dtype, keepalive=w_dev)
     return run_tucker(state, mats, pre=pre, post=post, out_dtype=out_dtype, keepalive=w_dev)
+
+
+def gpe_strang_run(linear_cache, weights, psi, tau, steps):
+    """``steps`` consecutive :func:`gpe_strang_step` calls (the loop of problems.py:597-598).
+
+    Between two steps the closing half-phase of step k and the opening
+    half-phase of step k+1 run back to back inside the fused epilogue of the
+    last product (``repeat = 2``), so only the very first half-phase is a
+    standalone pass.  Each rotation recomputes the density from the rotated
+    value, so the result is bitwise that of the step-by-step loop.
+    """
+    po = _Operand(psi)
+    if po.shape != linear_cache.shape:
+        raise ShapeError(f"state shape {po.shape} does not match cache shape {linear_cache.shape}")
+    _check_weights(weights, po.shape)
+    if steps < 1:
+        raise ConfigurationError("need at least one step")
+    if len(po.shape) > _native.MAX_D or len(po.shape) < 2:
+        raise ConfigurationError(f"the fused Strang run supports 2..{_native.MAX_D} directions")
+    out_dtype = _strang_dtype(po.dtype, linear_cache)
+    dev = po.obj.device if po.is_tensor and po.obj.is_cuda else dv.device()
+    w_dev = [dv.cached_vector(w, np.float64, dev) for w in weights]
+    inner_dev = dv.cached_vector(_inner_weight_product(weights, po.shape), np.float64, dev)
+    keep = w_dev + [inner_dev]
+    half_tau = 0.5 * tau
+    single = _gpe_op(po.shape, w_dev, half_tau, inner_dev, 1)
+    double = _gpe_op(po.shape, w_dev, half_tau, inner_dev, 2)
+    state = po.obj if po.is_tensor and po.obj.is_cuda else dv.to_device(np.asarray(po.obj), out_dtype, dev)
+    state = dv.tensor_as(state, out_dtype)
+    mats = _cache_mats(linear_cache, _Operand(state))
+    for k in range(steps):
+        pre = single if k == 0 else None
+        post = single if k == steps - 1 else double
+        state = run_tucker(state, mats, pre=pre, post=post, out_dtype=out_dtype, keepalive=keep)
+    if po.is_tensor and po.obj.is_cuda:
+        return state
+    return dv.to_host(state)
 
 
 def sin2_integral(t_a, t_b):

@@ -153,7 +153,9 @@ def launch_product(src_ptr, src_code, mat_ptr, mat_code, dst_ptr, m, nl, nmu, nr
     if src_code == _native.KM_C64 and mat_code == _native.KM_C64 and op is None:
         need = ctypes.c_size_t(0)
         _native.check(lib.km_tc_workspace_bytes(m, nmu, ctypes.byref(need)))
-        key = str(dev)
+        # one workspace per (device, stream): calls on one stream are ordered, so
+        # the factor planes of consecutive products may share it
+        key = (str(dev), stream.value if isinstance(stream, ctypes.c_void_p) else stream)
         buf = _TC_WORKSPACE.get(key)
         if buf is None or buf.numel() < need.value:
             buf = dv.torch.empty(need.value, dtype=dv.torch.uint8, device=dev)

@@ -370,3 +370,33 @@ def test_torch_tensors_stay_on_device():
     out = km.step(cache, t)
     assert isinstance(out, torch.Tensor) and out.is_cuda and dv.is_fortran(out)
     assert rel(dv.to_host(out), orc.step(cache.exps, u)) <= 1e-12
+
+
+def test_gpe_strang_run_equals_step_loop():
+    g = golden("gpe")
+    cache = km.PropagatorCache(0.1, tuple(g[f"gpe16__e{i}"] for i in range(3)))
+    ws = [g[f"gpe16__w{i}"] for i in range(3)]
+    run = km.gpe_strang_run(cache, ws, g["gpe16__psi0"], 0.1, 5)
+    assert rel(run, g["gpe16__out5"]) <= 1e-12
+    p = g["gpe16__psi0"]
+    for _ in range(5):
+        p = km.gpe_strang_step(cache, ws, p, 0.1)
+    assert np.array_equal(run, p)
+
+
+def test_gpe_strang_run_256_vs_step_loop():
+    import torch
+
+    from paper_2103_01691_b200 import _device as dv
+    from paper_2103_01691_b200.problems import weighted_vortex_state
+
+    n = 256
+    grids, lin_op, weights = km.gpe_setup(n)
+    psi = weighted_vortex_state(grids, weights)
+    cache = km.prepare(lin_op, 0.1)
+    t = dv.to_device(psi, np.complex128, torch.device("cuda", 0))
+    run = dv.to_host(km.gpe_strang_run(cache, weights, t, 0.1, 3))
+    p = t
+    for _ in range(3):
+        p = km.gpe_strang_step(cache, weights, p, 0.1)
+    assert np.array_equal(run, dv.to_host(p))
