@@ -187,9 +187,11 @@ def config5(budget, n=512):
     c64 = km.PropagatorCache(tau, tuple(e.astype(np.complex64) for e in cache.exps))
     p64 = dv.to_device(psi.astype(np.complex64), np.complex64, DEV)
     ms64 = dev_time(lambda: km.gpe_strang_step(c64, weights, p64, tau), 5)
+    ms_run = dev_time(lambda: km.gpe_strang_run(cache, weights, p_dev, tau, 4), 2, warm=1) / 4
     flop = 8 * 3 * n**4
     return {"config": "5: GPE 512^3 Strang step c128 (c64 input follows the reference's promotion to c128)",
-            "gpu_ms": ms, "gpu_ms_c64_input": ms64, "tflops": flop / (ms * 1e-3) / 1e12, "cpu_ms": cpu_ms,
+            "gpu_ms": ms, "gpu_ms_c64_input": ms64, "gpu_ms_per_step_fused_run": ms_run,
+            "tflops": flop / (ms * 1e-3) / 1e12, "cpu_ms": cpu_ms,
             "cpu_reps": kk, "speedup": cpu_ms / ms, "parity_rel_l2": orc.rel_l2(got, want)}
 
 
@@ -239,15 +241,33 @@ def config_magnus(budget, k=256, steps=4):
             "parity_rel_l2_device_vs_host_expm": orc.rel_l2(dv.to_host(devr), dv.to_host(host))}
 
 
+def config_c64(budget, n=256):
+    """Extra: the complex64 exact step (tcgen05 3xTF32 kernels) vs the reference's own complex64 path."""
+    u = crand(np.random.default_rng(0), (n,) * 3).astype(np.complex64)
+    c128 = schrod(n)
+    cache = km.PropagatorCache(0.01, tuple(e.astype(np.complex64) for e in c128.exps))
+    t = dv.to_device(u, np.complex64, DEV)
+    ms = dev_time(lambda: km.step(cache, t), 20)
+    got = km.step(cache, u)
+    want = orc.step(cache.exps, u)
+    want128 = orc.step(c128.exps, u.astype(np.complex128))
+    cpu_ms, kk = cpu_time(lambda: orc.step(cache.exps, u), budget, 3)
+    flop = 8 * 3 * n**4
+    return {"config": "extra: 3D Schrodinger 256^3 complex64 exact step (tcgen05 kind::tf32, 3xTF32)", "gpu_ms": ms,
+            "tflops": flop / (ms * 1e-3) / 1e12, "cpu_ms": cpu_ms, "cpu_reps": kk, "speedup": cpu_ms / ms,
+            "parity_rel_l2_vs_reference_c64": orc.rel_l2(got, want),
+            "rel_l2_vs_c128": orc.rel_l2(got, want128), "reference_c64_rel_l2_vs_c128": orc.rel_l2(want, want128)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--out", default=None)
-    ap.add_argument("--only", default="12345")
+    ap.add_argument("--only", default="12345ms")
     args = ap.parse_args()
     cores = os.cpu_count() or 1
     res = {"cores": cores, "configs": []}
-    fns = {"1": config1, "2": config2, "3": config3, "4": config4, "5": config5, "m": config_magnus}
+    fns = {"1": config1, "2": config2, "3": config3, "4": config4, "5": config5, "m": config_magnus, "s": config_c64}
     with threadpool_limits(limits=cores):
         for key in args.only:
             t0 = time.time()
