@@ -227,7 +227,8 @@ def run_ours(args):
         mats = cache.device_exps((np.complex128,) * 3, dev)
         runner = dist.LocalStepper(state, mats)
     else:
-        runner = dist.SlabStepper.from_global(u_host, cache, dev)
+        cls = dist.PeerSlabStepper if args.exchange == "peer" else dist.SlabStepper
+        runner = cls.from_global(u_host, cache, dev)
 
     for _ in range(max(args.warmup, 3)):
         runner.step()
@@ -309,7 +310,8 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "complex128",
             "data": "synthetic (seeded normal complex tensor, host-built expm factors)",
-            "config": dict(WORKLOAD, parallelism=("single GPU" if world == 1 else f"slab{world} along direction 3")),
+            "config": dict(WORKLOAD, parallelism=("single GPU" if world == 1 else
+                                                  f"slab{world} along direction 3, {args.exchange} exchange")),
             "gflops": value * FLOP_PER_STEP / 1e9,
             "roofline": roof,
             "cpu_baseline": cb,
@@ -331,6 +333,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--exchange", choices=["nccl", "peer"], default="nccl",
+                    help="multi-GPU all-to-all: NCCL, or fused into the products via NVLink peer stores")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -117,6 +117,25 @@ int km_mumode_split(const void* u, int u_dtype, const void* L, int L_dtype, void
                     int64_t out_block_stride, void* stream);
 
 /*
+ * μ-mode product whose output blocks are stored straight into other ranks'
+ * receive buffers (peer device pointers, e.g. NVLink-mapped symmetric
+ * memory): the all-to-all of the slab decomposition fused into the product's
+ * epilogue, so the exchange overlaps the math tile by tile.
+ * Exactly one blocking applies:
+ *   - out_block < m (n_left > 1): output rows [b*out_block, (b+1)*out_block)
+ *     go to peers[b] + peer_offset, laid out as the plain
+ *     (n_left, out_block, n_right) column-major block;
+ *   - fiber_block > 0 (n_left == 1): fibers [b*fiber_block, (b+1)*fiber_block)
+ *     go to peers[b] + peer_offset, as the (m, fiber_block) block.
+ * in_block / in_block_stride as in km_mumode_split.  Offsets are in elements.
+ * The caller orders the peers' writes before the reads (a device barrier).
+ */
+int km_mumode_peer(const void* u, int u_dtype, const void* L, int L_dtype, int64_t m,
+                   int64_t n_left, int64_t n_mu, int64_t n_right, int32_t in_block,
+                   int64_t in_block_stride, int32_t out_block, int64_t fiber_block,
+                   void* const* peers, int32_t npeers, int64_t peer_offset, void* stream);
+
+/*
  * complex64 x complex64 μ-mode product on the 5th-generation tensor cores
  * (tcgen05.mma kind::tf32, TMEM accumulator, 3xTF32 split for fp32-level
  * accuracy).  Same arguments as km_mumode plus a device workspace of at least

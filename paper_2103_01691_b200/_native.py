@@ -31,6 +31,7 @@ EXPORTS = (
     "km_last_error",
     "km_mumode",
     "km_mumode_split",
+    "km_mumode_peer",
     "km_tucker",
     "km_tucker_workspace",
     "km_pointwise",
@@ -74,6 +75,9 @@ def _declare(lib):
     lib.km_mumode_split.restype = c_int
     lib.km_mumode_split.argtypes = [c_vp, c_int, c_vp, c_int, c_vp, c_i64, c_i64, c_i64, c_i64,
                                     ctypes.c_int32, c_i64, ctypes.c_int32, c_i64, c_vp]
+    lib.km_mumode_peer.restype = c_int
+    lib.km_mumode_peer.argtypes = [c_vp, c_int, c_vp, c_int, c_i64, c_i64, c_i64, c_i64, ctypes.c_int32, c_i64,
+                                   ctypes.c_int32, c_i64, ctypes.POINTER(c_vp), ctypes.c_int32, c_i64, c_vp]
     lib.km_tucker.restype = c_int
     lib.km_tucker.argtypes = [
         c_vp, c_int, c_int, ctypes.POINTER(c_i64), ctypes.POINTER(c_vp), ctypes.POINTER(c_int),

@@ -113,18 +113,27 @@ int mumode_impl(const void* u, int udt, const void* L, int ldt, void* out, int64
   const int N = static_cast<int>(m), K = static_cast<int>(nmu);
   Split sp{K, 0, N, 0};
   if (split) {
-    const bool ksplit = split->kcb != K, nsplit = split->ncb != N;
+    const bool ksplit = split->kcb != K, nsplit = split->ncb != N, fsplit = split->fcb > 0;
     if (split->kcb < 1 || split->kcb > K || split->ncb < 1 || split->ncb > N)
       return fail(KM_EINVAL, "km_mumode_split: block sizes (%d, %d) outside (1..%d, 1..%d)", split->kcb,
                   split->ncb, K, N);
     if ((ksplit || nsplit) && nl == 1)
       return fail(KM_EINVAL, "km_mumode_split: blocked layouts need n_left > 1");
+    if (fsplit && (nl != 1 || nsplit || !split->peer[0]))
+      return fail(KM_EINVAL, "km_mumode_peer: fiber blocks need n_left == 1, unsplit rows and peer outputs");
     if (ksplit && split->kcb % BK != 0)
       return fail(KM_EINVAL, "km_mumode_split: input block %d is not a multiple of %d", split->kcb, BK);
     if (nsplit && split->ncb % 8 != 0)
       return fail(KM_EINVAL, "km_mumode_split: output block %d is not a multiple of 8", split->ncb);
-    if ((ksplit || nsplit) && op.kind != KM_OP_NONE)
+    if ((ksplit || nsplit || fsplit) && op.kind != KM_OP_NONE)
       return fail(KM_EINVAL, "km_mumode_split: pointwise ops are not supported on blocked layouts");
+    if (split->peer[0]) {
+      const int64_t blocks = fsplit ? (M + split->fcb - 1) / split->fcb : (N + split->ncb - 1) / split->ncb;
+      if (blocks > MAX_PEERS) return fail(KM_EINVAL, "km_mumode_peer: %lld output blocks exceed %d peers",
+                                          (long long)blocks, MAX_PEERS);
+      for (int64_t b = 0; b < blocks; ++b)
+        if (!split->peer[b]) return fail(KM_EINVAL, "km_mumode_peer: peer %lld is NULL", (long long)b);
+    }
     sp = *split;
     if (!ksplit) sp.kbs = 0;
     if (!nsplit) sp.nbs = 0;
@@ -270,6 +279,17 @@ int km_mumode_c64_tc(const void* u, const void* L, void* out, int64_t m, int64_t
     if (rc >= 0) return rc;
   }
   return mumode_impl(u, KM_C64, L, KM_C64, out, m, n_left, n_mu, n_right, nullptr, st);
+}
+
+int km_mumode_peer(const void* u, int u_dtype, const void* L, int L_dtype, int64_t m, int64_t n_left, int64_t n_mu,
+                   int64_t n_right, int32_t in_block, int64_t in_block_stride, int32_t out_block,
+                   int64_t fiber_block, void* const* peers, int32_t npeers, int64_t peer_offset, void* stream) {
+  if (!peers || npeers < 1 || npeers > MAX_PEERS)
+    return fail(KM_EINVAL, "km_mumode_peer: need 1..%d peer buffers, got %d", MAX_PEERS, npeers);
+  Split sp{in_block, in_block_stride, out_block, 0, static_cast<int>(fiber_block), peer_offset, {}};
+  for (int b = 0; b < npeers; ++b) sp.peer[b] = peers[b];
+  return mumode_impl(u, u_dtype, L, L_dtype, peers[0], m, n_left, n_mu, n_right, nullptr,
+                     static_cast<cudaStream_t>(stream), &sp);
 }
 
 int km_tucker_workspace(int u_dtype, int d, const int64_t* dims, const void* const* mats, const int* mat_dtypes,

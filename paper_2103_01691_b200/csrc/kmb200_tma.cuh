@@ -282,13 +282,29 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
     for (int i = 0; i < 4; ++i) {
       const int64_t f = m0 + wm + i * 8 + g;
       if (f >= M) continue;
-      const int64_t ob = KC ? f * N : (f % nl) + (f / nl) * nl * sp.ncb;
+      using TO = typename El<double, CU || CL>::T;
       const int64_t cs = KC ? 1 : nl;
+      TO* obase = out;
+      int64_t ob;
+      if constexpr (KC) {
+        if (sp.fcb) {  // fiber blocks to peers
+          const int64_t fb = f / sp.fcb;
+          obase = static_cast<TO*>(sp.peer[fb]) + sp.peer_off;
+          ob = (f - fb * sp.fcb) * N;
+        } else {
+          ob = f * N;
+        }
+      } else {
+        ob = (f % nl) + (f / nl) * nl * sp.ncb;
+      }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int c8 = n0 + wn + j * 8;
         const int nblk = KC ? 0 : c8 / sp.ncb;
-        const int64_t obj = ob + (KC ? 0 : nblk * sp.nbs) - static_cast<int64_t>(nblk) * sp.ncb * cs;
+        TO* dst = obase;
+        int64_t obj = ob - static_cast<int64_t>(nblk) * sp.ncb * cs;
+        if (!KC && sp.peer[0]) dst = static_cast<TO*>(sp.peer[nblk]) + sp.peer_off;
+        else if (!KC) obj += nblk * sp.nbs;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int col = c8 + 2 * t + h;
@@ -299,7 +315,7 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
             if (split_op) apply_op_split<OPK>(op, f, col, re, im);
             else apply_op<OPK>(op, p, re, im);
           }
-          out[p] = narrow<typename El<double, CU || CL>::T>(re, im);
+          dst[p] = narrow<TO>(re, im);
         }
       }
     }

@@ -208,6 +208,72 @@ class SlabStepper:
         return None
 
 
+class PeerSlabStepper(SlabStepper):
+    """:class:`SlabStepper` with the all-to-all fused into the products.
+
+    The last product before each exchange stores its per-peer output blocks
+    straight into the other ranks' receive buffers (``km_mumode_peer``: the
+    epilogue's stores go over NVLink to symmetric-memory peer pointers), so
+    the exchange overlaps the math tile by tile and no send buffer, pack pass
+    or NCCL call is needed; a device-side barrier then orders the peers'
+    writes before the local reads.  Receive buffers alternate between even and
+    odd steps, so one barrier per step suffices: a rank writes a peer's buffer
+    of parity p only after everybody passed the barrier of the step in
+    between, i.e. after the peer has consumed it.
+    """
+
+    def __init__(self, plan, rank, local_a, mats, recv_pair, peer_ptrs, barrier):
+        super().__init__(plan, rank, local_a, mats, comm=None)
+        self.send = None
+        self.recv_pair = recv_pair
+        self.peer_ptrs = [(ctypes.c_void_p * plan.P)(*ptrs) for ptrs in peer_ptrs]
+        self.barrier = barrier
+
+    @classmethod
+    def from_global(cls, u_host, cache, dev, group=None):
+        import torch.distributed as tdist
+        import torch.distributed._symmetric_memory as symm
+
+        group = group or tdist.group.WORLD
+        rank, P = tdist.get_rank(group), tdist.get_world_size(group)
+        plan = SlabPlan(u_host.shape, P)
+        local = dv.to_device(np.asfortranarray(plan.slab_a(u_host, rank)), np.complex128, dev)
+        mats = cache.device_exps((np.complex128,) * 3, dev)
+        if hasattr(symm, "enable_symm_mem_for_group"):
+            symm.enable_symm_mem_for_group(group.group_name)
+        bufs = [symm.empty(plan.local, dtype=dv.torch.complex128, device=dev) for _ in range(2)]
+        handles = [symm.rendezvous(b, group) for b in bufs]
+        ptrs = [list(h.buffer_ptrs) for h in handles]
+        st = cls(plan, rank, dv.as_fortran(local).permute(2, 1, 0).reshape(-1), mats, tuple(bufs), ptrs,
+                 lambda: handles[0].barrier(channel=0))
+        st._handles = handles  # keep the mappings alive
+        return st
+
+    def pre_exchange(self):
+        even = self.layout == "A"
+        before, _ = self.plan.even_calls() if even else self.plan.odd_calls()
+        self._run(before[:1], self.a, self.w, None)
+        mu, m, nl, nmu, nr, kcb, kbs, ncb, nbs = before[1]
+        # even: direction-2 rows in blocks of c2; odd: direction-1 fibers in blocks of c2*c3
+        out_block, fiber_block = (ncb, 0) if even else (m, self.plan.c2 * self.plan.c3)
+        _native.check(self.lib.km_mumode_peer(
+            self.w.data_ptr(), self.code, self.mats[mu].data_ptr(), self.mcodes[mu], m, nl, nmu, nr, kcb, kbs,
+            out_block, fiber_block, self.peer_ptrs[0 if even else 1], self.plan.P, self.rank * self.plan.block,
+            dv.stream_ptr(self.a.device)))
+        return None
+
+    def post_exchange(self):
+        even = self.layout == "A"
+        _, after = self.plan.even_calls() if even else self.plan.odd_calls()
+        self._run(after, self.recv_pair[0 if even else 1], self.a, self.w)
+        self.layout = "B" if even else "A"
+
+    def step(self):
+        self.pre_exchange()
+        self.barrier()
+        self.post_exchange()
+
+
 class NcclExchange:
     """Equal-split all-to-all of flat complex buffers over a torch.distributed group."""
 
@@ -232,16 +298,31 @@ class VirtualSlabGroup:
     while nothing waits on another process (SURVEY §4 "virtual-rank" test).
     """
 
-    def __init__(self, u_host, cache, dev, P):
+    def __init__(self, u_host, cache, dev, P, exchange="nccl"):
         self.plan = SlabPlan(u_host.shape, P)
+        self.exchange = exchange
         mats = cache.device_exps((np.complex128,) * 3, dev)
         self.ranks = []
+        locals_ = []
         for r in range(P):
             local = dv.to_device(np.asfortranarray(self.plan.slab_a(u_host, r)), np.complex128, dev)
-            flat = local.permute(2, 1, 0).reshape(-1)
-            self.ranks.append(SlabStepper(self.plan, r, flat, mats, comm=None))
+            locals_.append(local.permute(2, 1, 0).reshape(-1))
+        if exchange == "peer":
+            recv = [(dv.torch.empty_like(x), dv.torch.empty_like(x)) for x in locals_]
+            ptrs = [[recv[s][k].data_ptr() for s in range(P)] for k in range(2)]
+            for r in range(P):
+                self.ranks.append(PeerSlabStepper(self.plan, r, locals_[r], mats, recv[r], ptrs, lambda: None))
+        else:
+            for r in range(P):
+                self.ranks.append(SlabStepper(self.plan, r, locals_[r], mats, comm=None))
 
     def step(self):
+        if self.exchange == "peer":
+            for st in self.ranks:  # every rank stores its blocks into the others' receive buffers
+                st.pre_exchange()
+            for st in self.ranks:
+                st.post_exchange()
+            return
         P, bs = self.plan.P, self.plan.block
         sends = [st.pre_exchange() for st in self.ranks]
         for r, st in enumerate(self.ranks):

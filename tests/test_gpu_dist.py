@@ -53,8 +53,10 @@ def test_split_rejects_bad_blocks():
     assert lib.km_mumode_split(p, 3, p, 3, p, 16, 1, 32, 2, 16, 64, 16, 0, None) == _native.KM_EINVAL
 
 
-@pytest.mark.parametrize("P,n,steps", [(2, 64, 3), (4, 64, 4), (8, 256, 3)])
-def test_virtual_ranks_match_single_gpu(P, n, steps):
+@pytest.mark.parametrize("P,n,steps,exchange", [(2, 64, 3, "nccl"), (4, 64, 4, "nccl"), (8, 256, 3, "nccl"),
+                                                (2, 64, 3, "peer"), (4, 64, 4, "peer"), (8, 256, 3, "peer"),
+                                                (2, 256, 2, "peer")])
+def test_virtual_ranks_match_single_gpu(P, n, steps, exchange):
     import torch
 
     dev = torch.device("cuda", 0)
@@ -62,7 +64,7 @@ def test_virtual_ranks_match_single_gpu(P, n, steps):
     u = crand(rng, (n,) * 3)
     d2 = km.heat_factors(n, 2).factors[0]
     cache = km.prepare(km.KroneckerOp((1j * d2,) * 3), 0.01)
-    grp = dist.VirtualSlabGroup(u, cache, dev, P)
+    grp = dist.VirtualSlabGroup(u, cache, dev, P, exchange=exchange)
     for _ in range(steps):
         grp.step()
     got = grp.gather()

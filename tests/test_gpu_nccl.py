@@ -21,14 +21,14 @@ def _port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("n,steps", [(64, 3), (256, 2)])
-def test_slab_stepper_over_nccl(n, steps):
+@pytest.mark.parametrize("n,steps,exchange", [(64, 3, "nccl"), (256, 2, "nccl"), (64, 3, "peer"), (256, 2, "peer")])
+def test_slab_stepper_over_nccl(n, steps, exchange):
     import torch
 
     world = int(os.environ.get("KMB_SLAB_WORLD", str(min(torch.cuda.device_count(), 8))))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tools", "slab_check.py"), str(n), str(steps)]
+           os.path.join(ROOT, "tools", "slab_check.py"), str(n), str(steps), exchange]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "max_rel_l2" in r.stdout

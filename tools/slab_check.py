@@ -1,7 +1,7 @@
 """Run under torchrun (any world size): the NCCL slab stepper against a single-GPU
 reference computed on rank 0.  Exits non-zero on a parity failure.
 
-    torchrun --nproc-per-node P --master-addr 127.0.0.1 --master-port 29511 tools/slab_check.py [n] [steps]
+    torchrun --nproc-per-node P --master-addr 127.0.0.1 --master-port 29511 tools/slab_check.py [n] [steps] [nccl|peer]
 """
 import os
 import sys
@@ -18,6 +18,7 @@ from paper_2103_01691_b200 import _device as dv, dist  # noqa: E402
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 64
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+    exchange = sys.argv[3] if len(sys.argv) > 3 else "nccl"
     local = int(os.environ.get("LOCAL_RANK", "0"))
     ngpu = torch.cuda.device_count()
     dev = torch.device("cuda", local % ngpu)
@@ -28,7 +29,8 @@ def main():
     u = np.asfortranarray(rng.standard_normal((n,) * 3) + 1j * rng.standard_normal((n,) * 3))
     d2 = km.heat_factors(n, 2).factors[0]
     cache = km.prepare(km.KroneckerOp((1j * d2,) * 3), 0.01)
-    st = dist.SlabStepper.from_global(u, cache, dev)
+    cls = dist.PeerSlabStepper if exchange == "peer" else dist.SlabStepper
+    st = cls.from_global(u, cache, dev)
     for _ in range(steps):
         st.step()
     torch.cuda.synchronize()
@@ -42,7 +44,8 @@ def main():
     errs = torch.tensor([err], device=dev)
     tdist.all_reduce(errs, op=tdist.ReduceOp.MAX)
     if rank == 0:
-        print(f"slab_check world={world} n={n} steps={steps} layout={st.layout} max_rel_l2={errs.item():.3e}")
+        print(f"slab_check exchange={exchange} world={world} n={n} steps={steps} layout={st.layout} "
+              f"max_rel_l2={errs.item():.3e}")
     tdist.destroy_process_group()
     sys.exit(0 if errs.item() <= 1e-12 else 1)
 
