@@ -174,6 +174,18 @@ int km_tucker_workspace(int u_dtype, int d, const int64_t* dims, const void* con
 int km_pointwise(const void* in, void* out, int dtype, int64_t n, const km_pointop* op,
                  void* stream);
 
+/*
+ * Norms of a - b (b may be NULL) over n elements, result written to the
+ * device double *result (reference: tensor.norm, tensor.py:169-198, and
+ * relative_error, problems.py:160-169).  kind: 0 = max |.|, 1 = two-norm,
+ * 2 = weighted two-norm with the weight product of a KM_OP_GPE_PHASE-style
+ * km_pointop (weights[d-1] and inner_weights, dims).  Deterministic: fixed
+ * grid, fixed reduction order.  workspace >= km_norm_workspace_bytes().
+ */
+size_t km_norm_workspace_bytes(void);
+int km_norm(const void* a, const void* b, int dtype, int64_t n, int kind, const km_pointop* weights,
+            double* result, void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

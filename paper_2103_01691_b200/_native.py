@@ -38,6 +38,8 @@ EXPORTS = (
     "km_set_kernel_policy",
     "km_tc_workspace_bytes",
     "km_mumode_c64_tc",
+    "km_norm_workspace_bytes",
+    "km_norm",
 )
 
 
@@ -92,6 +94,10 @@ def _declare(lib):
     lib.km_tc_workspace_bytes.argtypes = [c_i64, c_i64, ctypes.POINTER(c_sz)]
     lib.km_mumode_c64_tc.restype = c_int
     lib.km_mumode_c64_tc.argtypes = [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_sz, c_vp]
+    lib.km_norm_workspace_bytes.restype = c_sz
+    lib.km_norm_workspace_bytes.argtypes = []
+    lib.km_norm.restype = c_int
+    lib.km_norm.argtypes = [c_vp, c_vp, c_int, c_i64, c_int, p_op, c_vp, c_vp, c_sz, c_vp]
     lib.km_set_kernel_policy.restype = c_int
     lib.km_set_kernel_policy.argtypes = [c_int]
     lib.km_pointwise.restype = c_int

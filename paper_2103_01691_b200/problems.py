@@ -33,7 +33,8 @@ from .errors import ConfigurationError, ShapeError
 from .fd import gpe_weighted_factors, sinh_clustered_grid
 from .hermite import position_operator
 from .kron import KroneckerOp, _cache_mats, prepare, step
-from .tensor import _Operand, run_tucker
+from .errors import InvalidReferenceError
+from .tensor import _Operand, device_norm, inner_weight_product, norm, run_tucker
 
 __all__ = [
     "VortexProfile",
@@ -42,6 +43,7 @@ __all__ = [
     "gpe_strang_step",
     "hkmp_factors",
     "magnus_midpoint_step",
+    "relative_error",
     "schrodinger_initial_state",
     "sin2_integral",
     "tdpot_phase_factor",
@@ -55,14 +57,7 @@ __all__ = [
 # pointwise operators handed to the C ABI
 
 
-def _inner_weight_product(weights, shape):
-    """w_1 ... w_{d-1} accumulated left to right as problems.py:528-539 does, flattened column-major."""
-    d = len(shape)
-    inner = np.ones(shape[:-1], order="F")
-    for ax, w in enumerate(weights[:-1]):
-        w = w.detach().cpu().numpy() if dv.is_tensor(w) else np.asarray(w, dtype=float)
-        inner *= w.reshape((1,) * ax + (w.size,) + (1,) * (d - 2 - ax))
-    return inner.reshape(-1, order="F")
+_inner_weight_product = inner_weight_product
 
 
 def _gpe_op(shape, weights_dev, half_tau, inner_dev=None, repeat=1):
@@ -178,6 +173,20 @@ def gpe_strang_run(linear_cache, weights, psi, tau, steps):
     if po.is_tensor and po.obj.is_cuda:
         return state
     return dv.to_host(state)
+
+
+def relative_error(u, ref, norm_kind="max", weights=None):
+    """``|u - ref| / |ref|`` in the chosen norm (problems.py:160-169), on the device.
+
+    The difference is formed inside the reduction kernel (no temporary tensor).
+    """
+    uo, ro = _Operand(u), _Operand(ref)
+    if uo.shape != ro.shape:
+        raise ShapeError(f"shapes {uo.shape} and {ro.shape} differ")
+    denom = norm(ref, norm_kind, weights)
+    if denom == 0.0:
+        raise InvalidReferenceError("reference tensor has zero norm")
+    return device_norm(uo.obj, norm_kind, weights, b=ro.obj) / denom
 
 
 def sin2_integral(t_a, t_b):

@@ -330,11 +330,60 @@ def tucker(u, mats):
     return run_tucker(uo.obj, mats)
 
 
+def inner_weight_product(weights, shape):
+    """w_1 ... w_{d-1} accumulated left to right (problems.py:528-539), flattened column-major."""
+    d = len(shape)
+    inner = np.ones(shape[:-1], order="F")
+    for ax, w in enumerate(weights[:-1]):
+        w = w.detach().cpu().numpy() if dv.is_tensor(w) else np.asarray(w, dtype=float)
+        inner *= w.reshape((1,) * ax + (w.size,) + (1,) * (d - 2 - ax))
+    return inner.reshape(-1, order="F")
+
+
+_NORM_KIND = {"max": 0, "two": 1, "weighted_two": 2}
+_NORM_WS = {}
+
+
+def device_norm(a, kind, weights=None, b=None):
+    """||a - b|| (b optional) through the ``km_norm`` kernels; ``a``/``b`` numpy or CUDA tensors."""
+    ao = _Operand(a)
+    dev = ao.obj.device if ao.is_tensor and ao.obj.is_cuda else dv.device()
+    dt = _compute_dtype(np.result_type(ao.dtype, *([] if b is None else [_Operand(b).dtype])))
+    ta = _tensor_on_device(ao, dt, dev)
+    tb = None if b is None else _tensor_on_device(_Operand(b), dt, dev)
+    lib = _native.lib()
+    key = str(dev)
+    ws = _NORM_WS.get(key)
+    if ws is None:
+        ws = dv.torch.empty(lib.km_norm_workspace_bytes() + 8, dtype=dv.torch.uint8, device=dev)
+        _NORM_WS[key] = ws
+    result = dv.torch.empty(1, dtype=dv.torch.float64, device=dev)
+    op = None
+    keep = []
+    if kind == "weighted_two":
+        shape = ao.shape if len(ao.shape) >= 2 else (1,) + tuple(ao.shape)
+        wl = list(weights) if len(ao.shape) >= 2 else [np.ones(1), weights[0]]
+        inner = dv.cached_vector(inner_weight_product(wl, shape), np.float64, dev)
+        last = dv.cached_vector(wl[-1], np.float64, dev)
+        keep = [inner, last]
+        op = _native.PointOp()
+        op.kind = _native.OP_GPE_PHASE
+        op.d = len(shape)
+        for i, n in enumerate(shape):
+            op.dims[i] = n
+        op.weights[len(shape) - 1] = last.data_ptr()
+        op.inner_weights = inner.data_ptr()
+    _native.check(lib.km_norm(ta.data_ptr(), None if tb is None else tb.data_ptr(), dv.code(dt), ta.numel(),
+                              _NORM_KIND[kind], None if op is None else ctypes.byref(op), result.data_ptr(),
+                              ws.data_ptr(), ws.numel(), dv.stream_ptr(dev)))
+    del keep
+    return float(result.item())
+
+
 def norm(u, kind="two", weights=None):
     """Tensor norm: ``max``, Euclidean ``two`` or ``weighted_two`` (tensor.py:169-198).
 
-    Reduced on the device (torch reductions; a fused epilogue reduction is the
-    SURVEY §8(f) row 3 follow-up).
+    One deterministic device reduction (``km_norm``: fixed grid, fixed order).
     """
     uo = _Operand(u)
     if kind not in ("max", "two", "weighted_two"):
@@ -351,21 +400,10 @@ def norm(u, kind="two", weights=None):
                     f"direction {mu}: weight vector of shape {wshape} does not match "
                     f"extent {uo.shape[mu - 1]}"
                 )
-    if uo.ndim and any(n == 0 for n in uo.shape):
+    if uo.ndim == 0:
+        return float(abs(np.asarray(uo.obj if not uo.is_tensor else uo.obj.cpu()).item()))
+    if any(n == 0 for n in uo.shape):
         if kind == "max":
             raise ValueError("zero-size array to reduction operation maximum which has no identity")
         return 0.0
-    dev = uo.obj.device if uo.is_tensor and uo.obj.is_cuda else dv.device()
-    t = _tensor_on_device(uo, _compute_dtype(uo.dtype), dev)
-    a = t.abs()
-    if kind == "max":
-        return float(a.max())
-    if kind == "two":
-        return float(dv.torch.linalg.vector_norm(t.reshape(-1) if t.is_contiguous() else t.flatten()))
-    acc = a * a
-    for mu, w in enumerate(weights):
-        wt = dv.cached_vector(w, np.float64, dev).to(acc.dtype)
-        shape = [1] * uo.ndim
-        shape[mu] = uo.shape[mu]
-        acc = acc * wt.reshape(shape)
-    return float(dv.torch.sqrt(acc.sum()))
+    return device_norm(uo.obj, kind, weights)

@@ -400,3 +400,36 @@ def test_gpe_strang_run_256_vs_step_loop():
     for _ in range(3):
         p = km.gpe_strang_step(cache, weights, p, 0.1)
     assert np.array_equal(run, dv.to_host(p))
+
+
+# ------------------------------------------------ device norms (km_norm)
+
+def test_relative_error_reference_semantics():
+    # test_problems.py:31-47
+    a = np.array([1.0, 2.0, 3.0])
+    assert km.relative_error(a, a) == 0.0
+    assert km.relative_error(2 * a, a, "two") == pytest.approx(1.0, rel=1e-15)
+    with pytest.raises(km.InvalidReferenceError):
+        km.relative_error(a, np.zeros(3))
+    with pytest.raises(km.ShapeError):
+        km.relative_error(a, np.ones(4))
+
+
+@pytest.mark.parametrize("kind", ["max", "two", "weighted_two"])
+def test_norms_large_vs_numpy(kind):
+    rng = np.random.default_rng(11)
+    shape = (96, 80, 70)
+    u = np.asfortranarray(rng.standard_normal(shape) + 1j * rng.standard_normal(shape))
+    ref = np.asfortranarray(u + 1e-3 * rng.standard_normal(shape))
+    ws = [rng.random(n) + 0.1 for n in shape]
+    if kind == "max":
+        want_n, want_e = np.abs(u).max(), np.abs(u - ref).max() / np.abs(ref).max()
+    elif kind == "two":
+        want_n, want_e = np.linalg.norm(u.ravel()), np.linalg.norm((u - ref).ravel()) / np.linalg.norm(ref.ravel())
+    else:
+        wp = orc.weight_product(ws, shape)
+        want_n = np.sqrt(np.sum(wp * np.abs(u) ** 2))
+        want_e = np.sqrt(np.sum(wp * np.abs(u - ref) ** 2)) / np.sqrt(np.sum(wp * np.abs(ref) ** 2))
+    w = ws if kind == "weighted_two" else None
+    assert km.norm(u, kind, w) == pytest.approx(want_n, rel=1e-13)
+    assert km.relative_error(u, ref, kind, w) == pytest.approx(want_e, rel=1e-12)

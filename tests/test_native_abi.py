@@ -16,7 +16,7 @@ HEADER = os.path.join(ROOT, "include", "kmb200.h")
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(km_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(km_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_the_binding_exports():
