@@ -158,6 +158,10 @@ int km_mumode_c64_tc(const void* u, const void* L, void* out, int64_t m, int64_t
  * mats[mu] == NULL skips that direction (tensor.py:164-165).  mats[mu] has
  * rows[mu] rows and dims[mu] columns.  ws0/ws1 are scratch buffers, each at
  * least the byte size of the largest intermediate (km_tucker_workspace()).
+ * ws1 may be NULL: `out` then doubles as the second ping-pong buffer, which
+ * needs every intermediate to fit in out (KM_EINVAL otherwise; always true
+ * for square factors), so a step costs one state-sized workspace.  The
+ * workspaces must not alias u, out or each other (KM_EINVAL).
  * pre is applied in a standalone pass, post is fused into the last product.
  */
 int km_tucker(const void* u, int u_dtype, int d, const int64_t* dims,

@@ -325,7 +325,6 @@ int km_tucker(const void* u, int u_dtype, int d, const int64_t* dims, const void
   int64_t n_in = 1;
   for (int i = 0; i < d; ++i) n_in *= dims[i];
 
-  const void* src = u;
   if (na == 0) {
     if (has_pre) {
       if ((rc = pointwise_impl(u, out, u_dtype, n_in, pre, st))) return rc;
@@ -336,14 +335,51 @@ int km_tucker(const void* u, int u_dtype, int d, const int64_t* dims, const void
     if (has_post) return pointwise_impl(out, out, fdt, n_in, post, st);
     return KM_OK;
   }
-  if (((na > 1 || has_pre) && !ws0) || (na > 1 && !ws1)) return fail(KM_EINVAL, "km_tucker: NULL workspace");
-  if (has_pre) {
-    void* dst = (na > 1) ? ws1 : ws0;
-    if ((rc = pointwise_impl(u, dst, u_dtype, n_in, pre, st))) return rc;
-    src = dst;
-  }
+  if ((na > 1 || has_pre) && !ws0) return fail(KM_EINVAL, "km_tucker: NULL workspace");
+  if ((ws0 && (ws0 == u || ws0 == out)) || (ws1 && (ws1 == u || ws1 == out || ws1 == ws0)))
+    return fail(KM_EINVAL, "km_tucker: a workspace aliases the input, the output or the other workspace");
+  // Destinations are assigned backwards from the last product (which writes
+  // out): ws0 and a second buffer alternate.  With ws1 == NULL the second
+  // buffer is `out` itself — legal because the product reading it never
+  // writes it — so a step needs one workspace, not two, when every
+  // intermediate fits in out (always true for square factors).
   int64_t cur[KM_MAX_D];
   for (int i = 0; i < d; ++i) cur[i] = dims[i];
+  size_t out_bytes = 0;
+  {
+    int64_t n = 1;
+    for (int i = 0; i < d; ++i) n *= (mats && mats[i]) ? rows[i] : dims[i];
+    out_bytes = static_cast<size_t>(n) * elem_bytes(fdt);
+  }
+  void* alt = ws1 ? ws1 : out;
+  void* dst[KM_MAX_D];
+  size_t dst_bytes[KM_MAX_D];
+  {
+    int64_t c[KM_MAX_D];
+    for (int i = 0; i < d; ++i) c[i] = dims[i];
+    int t = u_dtype;
+    for (int a = 0; a < na; ++a) {
+      c[active[a]] = rows[active[a]];
+      t = promote(t, mat_dtypes[active[a]]);
+      int64_t n = 1;
+      for (int i = 0; i < d; ++i) n *= c[i];
+      dst_bytes[a] = static_cast<size_t>(n) * elem_bytes(t);
+    }
+  }
+  dst[na - 1] = out;
+  for (int a = na - 2; a >= 0; --a) {
+    dst[a] = (dst[a + 1] == ws0) ? alt : ws0;
+    if (dst[a] == out && dst_bytes[a] > out_bytes)
+      return fail(KM_EINVAL, "km_tucker: intermediate %d does not fit in out; pass ws1", a + 1);
+  }
+  const void* src = u;
+  if (has_pre) {
+    void* pd = (dst[0] == ws0) ? alt : ws0;
+    if (pd == out && static_cast<size_t>(n_in) * elem_bytes(u_dtype) > out_bytes)
+      return fail(KM_EINVAL, "km_tucker: the pre-pass does not fit in out; pass ws1");
+    if ((rc = pointwise_impl(u, pd, u_dtype, n_in, pre, st))) return rc;
+    src = pd;
+  }
   int dt = u_dtype;
   for (int a = 0; a < na; ++a) {
     const int mu = active[a];
@@ -351,18 +387,16 @@ int km_tucker(const void* u, int u_dtype, int d, const int64_t* dims, const void
     for (int i = 0; i < mu; ++i) nl *= cur[i];
     for (int i = mu + 1; i < d; ++i) nr *= cur[i];
     const bool last = (a == na - 1);
-    void* dst = last ? out : (src == ws0 ? ws1 : ws0);
-    if (!last && dst == nullptr) return fail(KM_EINVAL, "km_tucker: NULL workspace");
     km_pointop post_here;
     const km_pointop* pp = nullptr;
     if (last && has_post) {
       post_here = *post;
       pp = &post_here;
     }
-    if ((rc = mumode_impl(src, dt, mats[mu], mat_dtypes[mu], dst, rows[mu], nl, cur[mu], nr, pp, st))) return rc;
+    if ((rc = mumode_impl(src, dt, mats[mu], mat_dtypes[mu], dst[a], rows[mu], nl, cur[mu], nr, pp, st))) return rc;
     dt = promote(dt, mat_dtypes[mu]);
     cur[mu] = rows[mu];
-    src = dst;
+    src = dst[a];
   }
   return KM_OK;
 }

@@ -2,8 +2,9 @@
 
 * :class:`LocalStepper` — one GPU.  The exact step ``u x_1 E_1 ... x_d E_d``
   runs as one ``km_tucker`` call per step over three device buffers (state,
-  one scratch, next state): the reference's acceptance criterion 9 bound of
-  3x the state (test_acceptance.py:298-321) holds on the device.
+  one scratch, next state; the next-state buffer doubles as the second
+  scratch): the reference's acceptance criterion 9 bound of 3x the state
+  (test_acceptance.py:298-321) holds on the device.
 * :class:`SlabStepper` — several GPUs, one process per GPU (torch.distributed
   over NCCL).  See the class docstring.
 """
@@ -40,11 +41,11 @@ class LocalStepper:
         self.lib = _native.lib()
 
     def step(self):
-        """``a <- a x_1 E_1 ... x_d E_d``; the input buffer doubles as the second scratch."""
+        """``a <- a x_1 E_1 ... x_d E_d``; the output buffer doubles as the second scratch."""
         stream = dv.stream_ptr(self.a.device)
         _native.check(self.lib.km_tucker(
             self.a.data_ptr(), self.code, self.d, self._c_dims, self._c_mats, self._c_codes, self._c_rows,
-            self.b.data_ptr(), self.w.data_ptr(), self.a.data_ptr(),
+            self.b.data_ptr(), self.w.data_ptr(), None,
             None if self.pre is None else ctypes.byref(self.pre),
             None if self.post is None else ctypes.byref(self.post), stream))
         self.a, self.b = self.b, self.a

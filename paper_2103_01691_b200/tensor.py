@@ -237,7 +237,9 @@ def run_tucker(u, mats, pre=None, post=None, out_dtype=None, keepalive=()):
         nact = sum(t is not None for t in mats_dev)
         need = ws.value if (nact > 1 or pre is not None) else 0
         ws0 = dv.torch.empty(max(need, 1), dtype=dv.torch.uint8, device=dev) if need else None
-        ws1 = dv.torch.empty(max(need, 1), dtype=dv.torch.uint8, device=dev) if need and nact > 1 else None
+        # out doubles as the second ping-pong buffer when every intermediate fits in it
+        fits = need <= out.numel() * out.element_size()
+        ws1 = dv.torch.empty(max(need, 1), dtype=dv.torch.uint8, device=dev) if need and nact > 1 and not fits else None
         _native.check(
             lib.km_tucker(
                 u_dev.data_ptr(), u_code, d, c_dims, c_mats, c_codes, c_rows, out.data_ptr(),

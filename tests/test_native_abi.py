@@ -112,3 +112,21 @@ def test_missing_library_fails_loudly(monkeypatch):
     monkeypatch.setattr(_native, "LIB_PATH", "/nonexistent/libkmb200.so")
     with pytest.raises(km.NativeLibraryError):
         _native.lib()
+
+
+def test_tucker_buffer_rules_checked_before_launch():
+    """ws1 == NULL reuses out as scratch only when the intermediates fit; no aliasing."""
+    lib = _native.lib()
+    d = 3
+    dims = (ctypes.c_int64 * d)(16, 8, 4)
+    mats = (ctypes.c_void_p * d)(1, 1, 1)
+    codes = (ctypes.c_int * d)(_native.KM_C128, _native.KM_C128, _native.KM_C128)
+    rows = (ctypes.c_int64 * d)(32, 8, 2)
+    u, out, w0, w1 = (ctypes.c_void_p(a) for a in (0x1000, 0x2000, 0x3000, 0x4000))
+    # products 1 and 3 would both write out, but the (32, 8, 4) intermediate is larger than the
+    # (32, 8, 2) result: out cannot stand in for ws1
+    rc = lib.km_tucker(u, _native.KM_C128, d, dims, mats, codes, rows, out, w0, None, None, None, None)
+    assert rc == _native.KM_EINVAL and b"does not fit" in lib.km_last_error()
+    for ws0, ws1 in ((u, w1), (w0, u), (w0, out), (w0, w0)):
+        rc = lib.km_tucker(u, _native.KM_C128, d, dims, mats, codes, rows, out, ws0, ws1, None, None, None)
+        assert rc == _native.KM_EINVAL and b"aliases" in lib.km_last_error()
