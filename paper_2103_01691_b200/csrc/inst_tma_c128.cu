@@ -103,7 +103,8 @@ int launch_tma_f64(const void* u, const void* L, void* out, int64_t M, int N, in
     if (!make_map(&ma, u, 5, dims, strides, box)) return -1;
   }
   const bool ops = op.kind != KM_OP_NONE;
-  if (ops && (kc || !(complex_tensor && complex_factor))) return -1;  // fused ops: c x c, strided layout only
+  // fused ops: c x c, strided layout, and only where (fiber, row) is the op's (l, i_last) split
+  if (ops && (kc || !(complex_tensor && complex_factor) || !op_split_ok(op, M, nl))) return -1;
   if (!complex_tensor) {
     if (complex_factor) {
       if (kc) return launch<true, KM_OP_NONE, true, false>(ma, mb, out, M, N, K, nl, op, sp, st);

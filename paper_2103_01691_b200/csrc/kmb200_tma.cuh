@@ -277,11 +277,13 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
     }
 
     // epilogue (overlaps the producer's loads for the next tile)
-    const bool split_op = (OPK != KM_OP_NONE) && !KC && op_split_ok(op, M, nl);
+    // fused ops run only where the host checked op_split_ok (inst_tma_c128.cu)
+    const SplitOpCtx octx = split_ctx<OPK>(op);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int64_t f = m0 + wm + i * 8 + g;
       if (f >= M) continue;
+      const double lf = split_fiber_weight<OPK>(op, f);
       using TO = typename El<double, CU || CL>::T;
       const int64_t cs = KC ? 1 : nl;
       TO* obase = out;
@@ -312,8 +314,7 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
           const int64_t p = obj + static_cast<int64_t>(col) * cs;
           double re = cr[i][j][h], im = (CU || CL) ? ci[i][j][h] : 0.0;
           if constexpr (OPK != KM_OP_NONE && (CU || CL)) {
-            if (split_op) apply_op_split<OPK>(op, f, col, re, im);
-            else apply_op<OPK>(op, p, re, im);
+            apply_op_fast<OPK>(op, octx, lf, col, re, im);
           }
           dst[p] = narrow<TO>(re, im);
         }
