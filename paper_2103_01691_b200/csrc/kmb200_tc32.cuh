@@ -290,14 +290,12 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
       for (int kt = 0; kt < KT; ++kt, ++q) {
         const int s = static_cast<int>(q % ST);
         tma::mbar_wait(&full[s], static_cast<unsigned>((q / ST) & 1));
-        [[maybe_unused]] const unsigned raw = sbase + s * STAGE_BYTES + OFF_B + tt * 16;
+        const unsigned raw = sbase + s * STAGE_BYTES + OFF_B + tt * 16;
         const unsigned lo = sbase + s * STAGE_BYTES + OFF_BLO + tt * 16;
         constexpr int J = PLANE_B / 16 / 128;
-#ifndef KMB_EXP_NO_SPLIT
         float4 x[J];
 #pragma unroll
         for (int j = 0; j < J; ++j) x[j] = tc32::lds_f4(raw + j * 2048);
-#ifndef KMB_EXP_RNA_HI
         // The tensor core reads an fp32 operand as tf32 by truncating the low 13
         // mantissa bits (verified: a rounding reader would leave ~5e-4 errors in
         // tests/test_gpu_tc32.py).  So the raw tile already is "hi" and only
@@ -310,16 +308,6 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
                                        __uint_as_float(__float_as_uint(x[j].w) & 0xFFFFE000u));
           tc32::sts_f4(lo + j * 2048, make_float4(x[j].x - h.x, x[j].y - h.y, x[j].z - h.z, x[j].w - h.w));
         }
-#else
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-          const float4 h =
-              make_float4(tc32::tf32_hi(x[j].x), tc32::tf32_hi(x[j].y), tc32::tf32_hi(x[j].z), tc32::tf32_hi(x[j].w));
-          tc32::sts_f4(raw + j * 2048, h);
-          tc32::sts_f4(lo + j * 2048, make_float4(x[j].x - h.x, x[j].y - h.y, x[j].z - h.z, x[j].w - h.w));
-        }
-#endif
-#endif
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) tma::mbar_arrive(&ready[s]);
