@@ -120,9 +120,14 @@ def to_device(a, dtype, dev):
     if a.ndim == 0:
         return torch.tensor(a.item(), dtype=torch_dtype(dtype), device=dev)
     host = torch.from_numpy(a)  # keeps the F strides, shares memory
+    if not host.is_pinned() and a.nbytes <= _STAGED_MAX:
+        return upload(a, dev)  # small pageable input: staged, no stream sync
     out = fortran_empty(a.shape, torch_dtype(dtype), dev)
     out.copy_(host, non_blocking=a.nbytes >= _PINNED_MIN and host.is_pinned())
     return out
+
+
+_STAGED_MAX = 16 << 20
 
 
 def tensor_as(t, dtype):
@@ -139,8 +144,68 @@ def matrix_to_device(m, dtype, dev):
     """Small matrix → C-contiguous (row-major) device tensor, as the C ABI wants."""
     if is_tensor(m):
         return m.to(device=dev, dtype=torch_dtype(dtype)).contiguous()
-    m = np.ascontiguousarray(np.asarray(m), dtype=dtype)
-    return torch.from_numpy(m).to(dev)
+    return upload(np.ascontiguousarray(np.asarray(m), dtype=dtype), dev)
+
+
+def upload(arr, dev):
+    """Host array → device tensor (same shape, strides and dtype) without a device sync.
+
+    A copy from pageable memory waits for all earlier work on the stream
+    before it starts; staging through page-locked memory instead makes
+    it an asynchronous DMA, so per-step host inputs (e.g. the Magnus
+    exponentials) queue behind the running products rather than stall the
+    host until they finish.  The staging blocks form a small ring; a block is
+    reused after the event of the copy that read it has completed (waiting
+    for the oldest one when all are busy, which bounds how far the host runs
+    ahead of the device).
+    """
+    arr = np.asarray(arr)
+    nbytes = arr.nbytes
+    f_order = arr.ndim > 1 and arr.flags.f_contiguous and not arr.flags.c_contiguous
+    if not (arr.flags.c_contiguous or f_order):
+        arr = np.ascontiguousarray(arr)
+    shape = arr.shape if not f_order else tuple(reversed(arr.shape))
+    out = torch.empty(shape, dtype=torch_dtype(arr.dtype), device=dev)
+    if f_order:
+        out = out.permute(*reversed(range(arr.ndim)))
+    if nbytes == 0:
+        return out
+    entry = _staging_block(nbytes)
+    stage = entry[0][:nbytes]
+    stage.numpy()[:] = arr.ravel(order="K").view(np.uint8)
+    flat = out.permute(*reversed(range(arr.ndim))) if f_order else out
+    flat.view(-1).view(torch.uint8).copy_(stage, non_blocking=True)
+    entry[1] = torch.cuda.Event()
+    entry[1].record(torch.cuda.current_stream(dev))
+    return out
+
+
+_STAGING = []  # ring of [pinned uint8 tensor, event of the copy that last read it (or None)]
+_STAGING_SLOTS = 16
+_STAGING_MIN = 1 << 20
+
+
+def _staging_block(nbytes):
+    def touch(e):  # move to the most-recently-used end (identity, not tensor ==)
+        _STAGING.pop(next(i for i, x in enumerate(_STAGING) if x is e))
+        _STAGING.append(e)
+        return e
+
+    fits = [e for e in _STAGING if e[0].numel() >= nbytes]
+    for e in fits:
+        if e[1] is None or e[1].query():
+            return touch(e)
+    if len(_STAGING) < _STAGING_SLOTS or not fits:
+        if len(_STAGING) >= _STAGING_SLOTS:  # no slot is large enough: retire the oldest
+            old = _STAGING.pop(0)
+            if old[1] is not None:
+                old[1].synchronize()
+        e = [torch.empty(max(nbytes, _STAGING_MIN), dtype=torch.uint8, pin_memory=True), None]
+        _STAGING.append(e)
+        return e
+    e = fits[0]  # all busy: wait for the least recently used one
+    e[1].synchronize()
+    return touch(e)
 
 
 _PINNED_MIN = 1 << 20
@@ -206,7 +271,7 @@ def cached_vector(v, dtype, dev):
     hit = _VEC_CACHE.get(key)
     if hit is not None:
         return hit
-    t = torch.from_numpy(arr).to(dev)
+    t = upload(arr, dev)
     if len(_VEC_CACHE) >= _VEC_CACHE_MAX:
         _VEC_CACHE.pop(next(iter(_VEC_CACHE)))
     _VEC_CACHE[key] = t
