@@ -25,18 +25,55 @@ template <typename T, int KIND>
 __global__ void __launch_bounds__(NORM_THREADS) norm_partial_kernel(const T* __restrict__ a, const T* __restrict__ b,
                                                                     int64_t n, const OpDev w, double* partials) {
   double acc = 0.0;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(NORM_THREADS) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * NORM_THREADS) {
-    const double2 x = load_diff(a, b, i);
-    if constexpr (KIND == 0) {
-      acc = fmax(acc, hypot(x.x, x.y));
-    } else {
-      double q = x.x * x.x + x.y * x.y;
-      if constexpr (KIND == 2) {
-        const int64_t il = i / w.inner;
-        q *= __ldg(w.winner + (i - il * w.inner)) * __ldg(w.w[w.d - 1] + il);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * NORM_THREADS;
+  int64_t i = blockIdx.x * static_cast<int64_t>(NORM_THREADS) + threadIdx.x;
+  if constexpr (KIND == 2) {
+    // (l, i_last) = (i mod inner, i / inner) advanced incrementally: one
+    // division per thread instead of one per element
+    const double* wl = w.w[w.d - 1];
+    const int64_t qs = stride / w.inner, rs = stride - qs * w.inner;
+    int64_t il = i / w.inner, l = i - il * w.inner;
+    auto advance = [&](int64_t& l_, int64_t& il_) {
+      l_ += rs;
+      il_ += qs;
+      if (l_ >= w.inner) {
+        l_ -= w.inner;
+        ++il_;
       }
-      acc += q;
+    };
+    for (; i + 3 * stride < n; i += 4 * stride) {  // four elements in flight, fixed fold order
+      double2 x[4];
+      double wt[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        x[j] = load_diff(a, b, i + j * stride);
+        wt[j] = __ldg(w.winner + l) * __ldg(wl + il);
+        advance(l, il);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc += (x[j].x * x[j].x + x[j].y * x[j].y) * wt[j];
+    }
+    for (; i < n; i += stride) {
+      const double2 x = load_diff(a, b, i);
+      acc += (x.x * x.x + x.y * x.y) * (__ldg(w.winner + l) * __ldg(wl + il));
+      advance(l, il);
+    }
+  } else {
+    // four independent loads in flight per thread, folded in a fixed order
+    for (; i + 3 * stride < n; i += 4 * stride) {
+      double2 x[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) x[j] = load_diff(a, b, i + j * stride);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if constexpr (KIND == 0) acc = fmax(acc, hypot(x[j].x, x[j].y));
+        else acc += x[j].x * x[j].x + x[j].y * x[j].y;
+      }
+    }
+    for (; i < n; i += stride) {
+      const double2 x = load_diff(a, b, i);
+      if constexpr (KIND == 0) acc = fmax(acc, hypot(x.x, x.y));
+      else acc += x.x * x.x + x.y * x.y;
     }
   }
   __shared__ double red[NORM_THREADS / 32];
@@ -54,12 +91,18 @@ __global__ void __launch_bounds__(NORM_THREADS) norm_partial_kernel(const T* __r
   }
 }
 
+// One warp: lane j folds partials j, j+32, ... in order, then a fixed
+// shuffle tree; the order never depends on timing.
 template <int KIND>
 __global__ void norm_final_kernel(const double* __restrict__ partials, int np, double* out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double r = 0.0;
-  for (int k = 0; k < np; ++k) r = KIND == 0 ? fmax(r, partials[k]) : r + partials[k];
-  out[0] = KIND == 0 ? r : sqrt(r);
+  for (int k = threadIdx.x; k < np; k += 32) r = KIND == 0 ? fmax(r, partials[k]) : r + partials[k];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double o = __shfl_down_sync(0xffffffffu, r, off);
+    r = KIND == 0 ? fmax(r, o) : r + o;
+  }
+  if (threadIdx.x == 0) out[0] = KIND == 0 ? r : sqrt(r);
 }
 
 int norm_blocks() { return 4 * num_sms(); }
