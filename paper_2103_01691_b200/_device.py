@@ -70,14 +70,6 @@ def stream_ptr(dev=None):
     return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
 
 
-def f_strides(shape):
-    strides, s = [], 1
-    for n in shape:
-        strides.append(s)
-        s *= int(n)
-    return tuple(strides)
-
-
 def is_fortran(t):
     """Column-major dense (size-1 extents may carry any stride)."""
     s = 1
