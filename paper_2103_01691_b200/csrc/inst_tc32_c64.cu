@@ -42,9 +42,29 @@ int launch(const CUtensorMap& ahi, const CUtensorMap& alo, const CUtensorMap& b,
     attr = true;
   }
   const int64_t fib_r = KC ? F : 2 * F;
-  const int64_t tiles = ((2 * m + tc32::BMR - 1) / tc32::BMR) * ((fib_r + tc32::BNR - 1) / tc32::BNR);
-  const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
-  kern<<<grid, tc32::THREADS, tc32::SMEM_BYTES, st>>>(ahi, alo, b, mo, F, m, K, nl);
+  // CTA pairs (cluster of 2): one pair per 256 E rows x 256 tensor columns
+  const int64_t tiles = ((2 * m + 2 * tc32::BMR - 1) / (2 * tc32::BMR)) * ((fib_r + tc32::BNR - 1) / tc32::BNR);
+  // not every SM can host half of a pair (TPCs with one usable SM): size the
+  // persistent grid by the clusters that are co-resident
+  static int max_pairs = 0;
+  if (max_pairs == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * (num_sms() / 2));
+    cfg.blockDim = dim3(tc32::THREADS);
+    cfg.dynamicSmemBytes = tc32::SMEM_BYTES;
+    cudaLaunchAttribute attr_c;
+    attr_c.id = cudaLaunchAttributeClusterDimension;
+    attr_c.val.clusterDim.x = 2;
+    attr_c.val.clusterDim.y = 1;
+    attr_c.val.clusterDim.z = 1;
+    cfg.attrs = &attr_c;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) n = num_sms() / 2;
+    max_pairs = n;
+  }
+  const int64_t pairs = tiles < max_pairs ? tiles : max_pairs;
+  kern<<<static_cast<unsigned>(2 * pairs), tc32::THREADS, tc32::SMEM_BYTES, st>>>(ahi, alo, b, mo, F, m, K, nl);
   return check_launch("mumode_tc32_kernel");
 }
 
@@ -90,7 +110,7 @@ int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t 
   if (kc) {
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(2 * K), static_cast<cuuint64_t>(F), 1};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(2 * K) * 4, static_cast<cuuint64_t>(2 * K) * 4 * F};
-    cuuint32_t box[3] = {tc32::BKR, tc32::BNR, 1};
+    cuuint32_t box[3] = {tc32::BKR, tc32::BNH, 1};  // each CTA of the pair stages half of the tile's columns
     if (!map_f32(&mb, u, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B)) return -1;
     // output (F x m complex, row-major in n): boxes of 32 fibers x 16 complex n
     CUtensorMap mo;
@@ -104,7 +124,7 @@ int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t 
                         1};
   cuuint64_t strides[4] = {static_cast<cuuint64_t>(nl) * 8, 128, static_cast<cuuint64_t>(nl) * K * 8,
                            static_cast<cuuint64_t>(nl) * K * 8 * nr};
-  cuuint32_t box[5] = {32, tc32::BKR, tc32::BNR / 32, 1, 1};
+  cuuint32_t box[5] = {32, tc32::BKR, tc32::BNH / 32, 1, 1};
   // MN-major tf32 operand: 32-B swizzle atoms (matches the BASE32B descriptor layout)
   if (!map_f32(&mb, u, 5, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return -1;
   // output (n_left x m x n_right complex): boxes of 16 fibers x 16 rows n

@@ -22,10 +22,20 @@
 // K' = 512 and keeps longer contractions on the DMMA path (1e-5 bar).  E's hi/lo planes are prepared once per call (prep_planes_kernel);
 // the tensor tile is split in shared memory by four transform warps.
 //
-// Warp roles (10 warps): 0 TMA producer, 1 MMA issuer + TMEM owner,
-// 2-5 hi/lo transform, 6-9 epilogue (TMEM -> registers -> global).  The grid is
-// persistent; the two 128-column TMEM accumulators are double-buffered so the
-// epilogue of tile i overlaps the MMAs of tile i+1.
+// CTA pairs (cta_group::2, cluster of 2): a tile is 256 real E rows x 256
+// tensor columns; each CTA stages its own 128 E rows and HALF of the tensor
+// columns, the leader CTA issues M = 256 / N = 256 MMAs that read both CTAs'
+// shared memory, and each CTA's TMEM receives its 128 rows x 256 columns.  The
+// tensor operand's shared-memory traffic per SM (TMA writes, hi/lo split, MMA
+// reads) halves; with one CTA per tile the kernel was bound by it (tensor pipe
+// 75 % of elapsed, now 86 %).
+//
+// Warp roles (10 warps per CTA): 0 TMA producer, 1 TMEM owner + MMA issuer
+// (leader CTA), 2-5 hi/lo transform of the CTA's tensor half, 6-9 epilogue
+// (TMEM -> registers -> global).  Split and epilogue warps of both CTAs arrive
+// on the leader's barriers; MMA completion is committed to both CTAs
+// (multicast).  The grid is persistent; the two 256-column TMEM accumulators
+// are double-buffered so the epilogue of tile i overlaps the MMAs of tile i+1.
 #pragma once
 #include "kmb200_tma.cuh"
 
@@ -33,15 +43,16 @@ namespace kmb {
 
 namespace tc32 {
 
-constexpr int BMR = 128;   // real rows of D per tile (64 complex rows of E)
-constexpr int BNR = 256;   // real columns of D per tile (one N=256 MMA)
+constexpr int BMR = 128;   // real rows of D per CTA (64 complex rows of E); a CTA pair covers 256
+constexpr int BNR = 256;   // real columns of D per tile (one N=256 MMA, shared by the pair)
+constexpr int BNH = BNR / 2;  // real columns of B each CTA of the pair stages (cta_group::2 splits N)
 constexpr int BKR = 16;    // real k per stage (64 B of fp32: SWIZZLE_64B K-major rows)
-constexpr int ST = 4;      // pipeline stages
+constexpr int ST = 6;      // pipeline stages
 constexpr int PLANE_A = BMR * BKR * 4;          // 8 KB: 128 x 16 fp32 (E hi or lo)
-constexpr int PLANE_B = BNR * BKR * 4;          // 16 KB: 256 x 16 fp32 (tensor raw->hi or lo)
+constexpr int PLANE_B = BNH * BKR * 4;          // 8 KB: 128 x 16 fp32 (tensor raw->hi or lo)
 constexpr int OFF_ALO = PLANE_A, OFF_B = 2 * PLANE_A, OFF_BLO = 2 * PLANE_A + PLANE_B;
 constexpr int STAGE_BYTES = 2 * PLANE_A + 2 * PLANE_B;
-constexpr int TX_BYTES = 2 * PLANE_A + PLANE_B;  // bytes TMA lands per stage
+constexpr int TX_BYTES = 2 * PLANE_A + PLANE_B;  // bytes TMA lands per stage and CTA
 constexpr int THREADS = 320;
 constexpr int XSTAGE = 32 * 128;  // per epilogue warp: one 32 x 32-float (KC) or 16 x 32 (MC) output box
 constexpr int SMEM_BYTES = ST * STAGE_BYTES + 1024 + 4 * XSTAGE + 1024;
@@ -59,25 +70,52 @@ __device__ __forceinline__ uint64_t desc_sw(unsigned saddr, unsigned lbo, unsign
   return d;
 }
 
-// kind::tf32, fp32 accumulate, A K-major, B K- or MN-major, M = 128, N = 128
+// kind::tf32, fp32 accumulate, A K-major, B K- or MN-major, M = 256 (the CTA
+// pair: 128 rows of A from each CTA), N = 256 (128 columns of B from each CTA)
 __host__ __device__ constexpr uint32_t idesc_tf32(bool b_mn_major) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((b_mn_major ? 1u : 0u) << 16) | ((BNR >> 3) << 17) |
-         ((BMR >> 4) << 24);
+         (((2 * BMR) >> 4) << 24);
 }
 
+// issued by one thread of the pair's leader CTA; reads A and B from both CTAs'
+// shared memory and writes each CTA's 128 accumulator rows into its own TMEM
 __device__ __forceinline__ void mma_tf32(uint32_t dtmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(dtmem),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
-__device__ __forceinline__ void commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                   tma::su32(bar))
-               : "memory");
+// MMA completion to the same barrier (offset) in both CTAs of the pair
+__device__ __forceinline__ void commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          tma::su32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+__device__ __forceinline__ unsigned cta_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+// arrive on the leader CTA's copy of a barrier.  The operands the MMA reads
+// were ordered for the tensor core's (async) proxy by fence.proxy.async /
+// tcgen05 fences before this; a cluster-scope release here would add a full
+// memory barrier per arrive (measured: it halved the kernel's throughput).
+__device__ __forceinline__ void arrive_leader(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 ra;\n"
+      "mapa.shared::cluster.u32 ra, %0, 0;\n"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n"
+      "}\n" ::"r"(tma::su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
@@ -166,11 +204,10 @@ __global__ void prep_planes_kernel(const float2* __restrict__ L, float* __restri
 }
 
 template <bool KC>
-__global__ void __launch_bounds__(tc32::THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc32::THREADS, 1)
     mumode_tc32_kernel(const __grid_constant__ CUtensorMap mapAhi, const __grid_constant__ CUtensorMap mapAlo,
                        const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapOut, int64_t F,
-                       int m, int K,
-                       int64_t nl) {
+                       int m, int K, int64_t nl) {
   using namespace tc32;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
@@ -184,48 +221,50 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
   unsigned char* xstage = smem + ST * STAGE_BYTES + 1024;  // 1024-B aligned (128-B swizzle)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned rank = cta_rank();  // 0 = leader of the CTA pair (issues the MMAs)
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
-      tma::mbar_init(&full[s], 1);
-      tma::mbar_init(&ready[s], 4);
-      tma::mbar_init(&empty[s], 1);
+      tma::mbar_init(&full[s], 1);    // this CTA's TMA bytes
+      tma::mbar_init(&ready[s], 8);   // leader: 4 split warps of each CTA
+      tma::mbar_init(&empty[s], 1);   // MMA commit (multicast to both CTAs)
     }
     for (int b = 0; b < 2; ++b) {
-      tma::mbar_init(&tfull[b], 1);
-      tma::mbar_init(&tempty[b], 4);
+      tma::mbar_init(&tfull[b], 1);   // MMA commit (multicast)
+      tma::mbar_init(&tempty[b], 8);  // leader: 4 epilogue warps of each CTA
     }
     tma::fence_barrier_init();
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tma::su32(tmem_slot)),
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tma::su32(tmem_slot)),
                  "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::);
   }
   fence_before();
-  __syncthreads();
+  cluster_sync();  // barriers initialised and TMEM allocated in both CTAs before any remote arrive
   fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int64_t fib_r = KC ? F : 2 * F;               // real columns of B
-  const int nE = (2 * m + BMR - 1) / BMR;             // tiles along E's real rows
-  const int64_t nF = (fib_r + BNR - 1) / BNR;         // tiles along the real columns
+  const int64_t fib_r = KC ? F : 2 * F;                // real columns of B
+  const int nE = (2 * m + 2 * BMR - 1) / (2 * BMR);    // pair tiles along E's real rows (256 each)
+  const int64_t nF = (fib_r + BNR - 1) / BNR;          // tiles along the real columns (256 each)
   const int64_t tiles = nE * nF;
-  const int KR = KC ? 2 * K : K;                      // real contraction length
+  const int64_t pair = blockIdx.x >> 1, pairs = gridDim.x >> 1;
+  const int KR = KC ? 2 * K : K;                       // real contraction length
   const int KT = (KR + BKR - 1) / BKR;
-  const int64_t my_tiles = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t my_tiles = tiles > pair ? (tiles - 1 - pair) / pairs + 1 : 0;
   const unsigned sbase = tma::su32(smem);
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producer (each CTA: its A rows, its B half)
     if (lane == 0) {
       tma::prefetch_map(&mapAhi);
       tma::prefetch_map(&mapAlo);
       tma::prefetch_map(&mapB);
       int64_t q = 0;
       for (int64_t it = 0; it < my_tiles; ++it) {
-        const int64_t tile = blockIdx.x + it * gridDim.x;
-        const int e0 = static_cast<int>(tile % nE) * BMR;
-        const int64_t c0 = (tile / nE) * BNR;
+        const int64_t tile = pair + it * pairs;
+        const int e0 = static_cast<int>(tile % nE) * 2 * BMR + static_cast<int>(rank) * BMR;
+        const int64_t c0 = (tile / nE) * BNR + rank * BNH;
         for (int kt = 0; kt < KT; ++kt, ++q) {
           const int s = static_cast<int>(q % ST);
           if (q >= ST) tma::mbar_wait(&empty[s], static_cast<unsigned>((q / ST - 1) & 1));
@@ -237,7 +276,7 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
           if constexpr (KC) {
             tma::load3(st + OFF_B, &mapB, &full[s], k0, static_cast<int>(c0), 0);
           } else {
-            const int64_t f0 = c0 / 2;  // fibers; the tile lies inside one n_left slab
+            const int64_t f0 = c0 / 2;  // fibers; the pair tile lies inside one n_left slab
             tma::load5(st + OFF_B, &mapB, &full[s], 0, k0, static_cast<int>((f0 % nl) / 16),
                        static_cast<int>(f0 / nl), 0);
           }
@@ -245,8 +284,8 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA only)
+    if (rank == 0 && lane == 0) {
       constexpr uint32_t idesc = idesc_tf32(!KC);
       int64_t q = 0;
       for (int64_t it = 0; it < my_tiles; ++it) {
@@ -277,13 +316,13 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
             mma_tf32(d, alo, bhi, idesc, 1u);
             mma_tf32(d, ahi, blo, idesc, 1u);
           }
-          commit(&empty[s]);
+          commit_pair(&empty[s]);
         }
-        commit(&tfull[b]);
+        commit_pair(&tfull[b]);
       }
     }
   } else if (warp < 6) {
-    // ------------------------------------------------------------ hi/lo split of the tensor tile
+    // ------------------------------------------------------------ hi/lo split of this CTA's tensor half
     const int tt = threadIdx.x - 64;  // 0..127
     int64_t q = 0;
     for (int64_t it = 0; it < my_tiles; ++it) {
@@ -310,19 +349,20 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
         }
         fence_proxy_async();
         __syncwarp();
-        if (lane == 0) tma::mbar_arrive(&ready[s]);
+        if (lane == 0) arrive_leader(&ready[s]);
       }
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    // TMEM -> registers -> swizzled shared staging (4 KB per warp) -> TMA store.
-    // The staging layout is the output box with the 128-B swizzle, so the
-    // staging writes are bank-conflict free (KC) or 2-way (MC).
+    // TMEM (this CTA's 128 rows x 256 columns) -> registers -> swizzled shared
+    // staging (4 KB per warp) -> TMA store.  The staging layout is the output
+    // box with the 128-B swizzle, so the staging writes are bank-conflict free
+    // (KC) or 2-way (MC).
     const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
     const unsigned stg = tma::su32(xstage) + (warp - 6) * XSTAGE;
     for (int64_t it = 0; it < my_tiles; ++it) {
-      const int64_t tile = blockIdx.x + it * gridDim.x;
-      const int e0 = static_cast<int>(tile % nE) * BMR;
+      const int64_t tile = pair + it * pairs;
+      const int e0 = static_cast<int>(tile % nE) * 2 * BMR + static_cast<int>(rank) * BMR;
       const int64_t c0 = (tile / nE) * BNR;
       const int b = static_cast<int>(it & 1);
       tma::mbar_wait(&tfull[b], static_cast<unsigned>((it >> 1) & 1));
@@ -364,13 +404,13 @@ __global__ void __launch_bounds__(tc32::THREADS, 1)
       }
       fence_before();
       __syncwarp();
-      if (lane == 0) tma::mbar_arrive(&tempty[b]);
+      if (lane == 0) arrive_leader(&tempty[b]);
     }
     if (lane == 0) tc32::bulk_wait_all();
   }
   fence_before();
-  __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  cluster_sync();  // the peer's MMAs and arrivals are done before TMEM goes away
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
 }  // namespace kmb
