@@ -140,7 +140,8 @@ int km_mumode_peer(const void* u, int u_dtype, const void* L, int L_dtype, int64
  * (tcgen05.mma kind::tf32, TMEM accumulator, 3xTF32 split for fp32-level
  * accuracy).  Same arguments as km_mumode plus a device workspace of at least
  * km_tc_workspace_bytes(m, n_mu) bytes (the factor's split planes).  Shapes
- * the kernel does not take (n_left > 1 with n_left % 64 != 0, n_mu % 4 != 0,
+ * the kernel does not take (n_left > 1 with n_left % 128 != 0, n_mu % 4 != 0,
+ * a contraction K' = 2*n_mu (n_left == 1) or n_mu (n_left > 1) above 512,
  * a too-small workspace, KM_POLICY_NO_TMA) run the DMMA path instead.
  */
 int km_tc_workspace_bytes(int64_t m, int64_t n_mu, size_t* bytes);
