@@ -72,10 +72,15 @@ typedef struct km_pointop {
   const double* inner_weights;
 } km_pointop;
 
-/* kernel selection (process-wide): AUTO picks the warp-specialised TMA
- * kernel for complex128 products whose shape allows it; NO_TMA forces the
- * cp.async kernel everywhere (A/B testing and verification) */
-enum km_kernel_policy { KM_POLICY_AUTO = 0, KM_POLICY_NO_TMA = 1 };
+/* kernel selection (process-wide, bit flags): AUTO picks the warp-specialised
+ * TMA kernels where the shape allows and balances their last wave with
+ * stream-K; NO_TMA forces the cp.async kernel everywhere; NO_STREAMK keeps
+ * whole tiles only (A/B testing and verification).  The stream-K tail keeps one
+ * internal scratch buffer per (device, stream), allocated on first use
+ * (~76 MB on 148 SMs).  Launches captured into a CUDA graph keep whole tiles:
+ * the partials' publish flags are per-launch epochs, which a replayed graph
+ * would repeat. */
+enum km_kernel_policy { KM_POLICY_AUTO = 0, KM_POLICY_NO_TMA = 1, KM_POLICY_NO_STREAMK = 2 };
 int km_set_kernel_policy(int policy);
 
 /* ABI version and build info */

@@ -3,7 +3,14 @@
 
 #include <cudaTypedefs.h>
 
+#include <cstring>
+#include <map>
+#include <mutex>
+
 namespace kmb {
+
+bool g_tma_disabled = false;
+bool g_streamk_disabled = false;
 
 namespace {
 
@@ -32,26 +39,106 @@ bool make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims
   return r == CUDA_SUCCESS;
 }
 
+// Stream-K scratch, one per (device, stream): partial accumulators and flags.
+// Allocated once at the largest size a launch can need (2 * SMs stream-K
+// tiles, 2 extra pieces each), so no launch reallocates; flags start at 0 and
+// every launch publishes under a fresh epoch.
+struct SkScratch {
+  double* part = nullptr;
+  unsigned* flags = nullptr;
+  unsigned epoch = 0;
+};
+
+SkScratch* sk_scratch(cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, SkScratch> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  SkScratch& s = cache[{dev, st}];
+  if (!s.part) {
+    const size_t pieces = static_cast<size_t>(2 * num_sms()) * 2 * tma::CONSUMERS;
+    if (cudaMalloc(&s.part, pieces * 2048 * sizeof(double)) != cudaSuccess) return nullptr;
+    if (cudaMalloc(&s.flags, pieces * sizeof(unsigned)) != cudaSuccess) return nullptr;
+    if (cudaMemset(s.flags, 0, pieces * sizeof(unsigned)) != cudaSuccess) return nullptr;
+  }
+  return &s;
+}
+
+template <typename Kern>
+int set_smem(Kern k) {
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tma::SMEM_BYTES);
+  return e == cudaSuccess ? KM_OK : fail(KM_ECUDA, "cudaFuncSetAttribute(tma): %s", cudaGetErrorString(e));
+}
+
+// Stream-K launch of a complex x complex product.  Returns -1 when the shape or
+// the stream does not call for it (the caller launches whole tiles).
+// Stream-K pays for products whose tiles make 1-4 waves with a partial last
+// one (e.g. the 256^3 state split over 4 or 8 GPUs): that wave plus one full
+// wave is cut into equal k-ranges, so every CTA's range holds at least KT
+// k-blocks.  Measured (tools/slab_probe.py): per-rank products at P = 4 / 8 go
+// from 0.80 / 0.78 to 0.88 / 0.83 of the DMMA peak.  Fewer tiles than SMs (the
+// 1024^2 real pipe-flow product) and many-wave launches measured no gain.
+template <bool KC, int OPK>
+int launch_streamk(const CUtensorMap& ma, const CUtensorMap& mb, double2* out, int64_t M, int N, int K, int64_t nl,
+                   const OpDev& op, const Split& sp, cudaStream_t st) {
+  const int64_t tiles = ((M + tma::BM - 1) / tma::BM) * ((N + tma::BN - 1) / tma::BN);
+  const int64_t KT = (K + tma::BKS - 1) / tma::BKS;
+  const int64_t S = num_sms();
+  if (g_streamk_disabled || tiles <= S || tiles % S == 0 || tiles > 4 * S || KT < 2) return -1;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cap);
+  if (cap != cudaStreamCaptureStatusNone) return -1;  // epochs would repeat on replay
+  StreamK sk;
+  memset(&sk, 0, sizeof(sk));
+  sk.dp_waves = tiles / S - 1;
+  sk.sk_base = sk.dp_waves * S;
+  sk.iters = (tiles - sk.sk_base) * KT;
+  const int64_t per = sk.iters / S;                      // >= KT: a tile spans at most 2 CTAs
+  sk.slots = static_cast<int>((KT + per - 1) / per);
+  SkScratch* scr = sk_scratch(st);
+  if (!scr) return -1;
+  auto kern = mumode_tma_kernel<KC, OPK, true, true, true>;
+  static bool attr = false;
+  if (!attr) {
+    if (int rc = set_smem(kern)) return rc;
+    attr = true;
+  }
+  sk.part = scr->part;
+  sk.flags = scr->flags;
+  sk.epoch = ++scr->epoch;
+  void* args[] = {const_cast<CUtensorMap*>(&ma), const_cast<CUtensorMap*>(&mb), &out, &M, &N, &K, &nl,
+                  const_cast<OpDev*>(&op), const_cast<Split*>(&sp), &sk};
+  cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(static_cast<unsigned>(S)),
+                                              dim3(tma::THREADS), args, tma::SMEM_BYTES, st);
+  return e == cudaSuccess ? KM_OK : fail(KM_ECUDA, "mumode_tma_kernel (stream-K): %s", cudaGetErrorString(e));
+}
+
 template <bool KC, int OPK, bool CL, bool CU>
 int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* out, int64_t M, int N, int K, int64_t nl,
            const OpDev& op, const Split& sp, cudaStream_t st) {
-  auto kern = mumode_tma_kernel<KC, OPK, CL, CU>;
+  using TO = typename El<double, CU || CL>::T;
+  if constexpr (CU && CL) {
+    const int rc = launch_streamk<KC, OPK>(ma, mb, static_cast<double2*>(out), M, N, K, nl, op, sp, st);
+    if (rc >= 0) return rc;
+  }
+  auto kern = mumode_tma_kernel<KC, OPK, CL, CU, false>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tma::SMEM_BYTES);
-    if (e != cudaSuccess) return fail(KM_ECUDA, "cudaFuncSetAttribute(tma): %s", cudaGetErrorString(e));
+    if (int rc = set_smem(kern)) return rc;
     attr = true;
   }
   const int64_t tiles = ((M + tma::BM - 1) / tma::BM) * ((N + tma::BN - 1) / tma::BN);
-  const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
-  kern<<<grid, tma::THREADS, tma::SMEM_BYTES, st>>>(ma, mb, static_cast<typename El<double, CU || CL>::T*>(out), M,
-                                                    N, K, nl, op, sp);
+  const int64_t S = num_sms();
+  StreamK none;
+  memset(&none, 0, sizeof(none));
+  const int grid = static_cast<int>(tiles < S ? tiles : S);
+  kern<<<grid, tma::THREADS, tma::SMEM_BYTES, st>>>(ma, mb, static_cast<TO*>(out), M, N, K, nl, op, sp, none);
   return check_launch("mumode_tma_kernel");
 }
 
 }  // namespace
 
-bool g_tma_disabled = false;
 
 int launch_tma_f64(const void* u, const void* L, void* out, int64_t M, int N, int K, int64_t nl, const OpDev& op,
                    const Split& sp, cudaStream_t st, bool complex_tensor, bool complex_factor) {

@@ -99,6 +99,25 @@ __device__ __forceinline__ void load5(void* dst, const CUtensorMap* m, uint64_t*
 
 }  // namespace tma
 
+// Stream-K tail (host: inst_tma_c128.cu).  The first dp_waves * gridDim.x
+// tiles are whole tiles, one CTA each; the k-blocks of the remaining tiles are
+// cut into gridDim.x equal contiguous ranges, one per CTA, so every CTA does the
+// same number of k-blocks.  A tile cut between CTAs is finished by the CTA
+// holding its first k-block (the "owner"): the others store their partial
+// accumulators (per warp, in piece order) with a release flag, and the owner
+// adds them in piece order, so the result does not depend on timing.  The
+// launch is cooperative (all CTAs resident), and a CTA only waits at the end
+// of its range, after its own partial pieces are published: no cycles.
+struct StreamK {
+  int64_t dp_waves;  // whole-tile waves before the stream-K range (0 when iters == 0: all tiles whole)
+  int64_t sk_base;   // first stream-K tile
+  int64_t iters;     // k-blocks in the stream-K range (0 = none)
+  double* part;      // partial accumulators: [sk tile][piece-1][warp][64 values][32 lanes]
+  unsigned* flags;   // [sk tile][piece-1][warp] == epoch once published
+  unsigned epoch;
+  int slots;         // pieces per tile - 1
+};
+
 // CL = false: real factor (e.g. the Hermite Φ), 2 DMMA per complex multiply-add.
 // Its box is (16 real k, 64 rows) in 128-B rows; one LDS.128 fetches the
 // factor values of two consecutive k-steps (k = 2c, 2c+1 share a 16-B chunk
@@ -108,11 +127,11 @@ __device__ __forceinline__ void load5(void* dst, const CUtensorMap* m, uint64_t*
 // boxes are (16 fibers, 16 k, 8 fiber groups) in 128-B rows and read with one
 // conflict-free LDS.64 per MMA tile; k-contiguous boxes are (16 k, 128 fibers)
 // and read in k pairs with LDS.128 like the real factor.
-template <bool KC, int OPK, bool CL = true, bool CU = true>
+template <bool KC, int OPK, bool CL = true, bool CU = true, bool SKT = false>
 __global__ void __launch_bounds__(tma::THREADS, 1)
     mumode_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                       typename El<double, CU || CL>::T* __restrict__ out, int64_t M, int N, int K, int64_t nl,
-                      const OpDev op, const Split sp) {
+                      const OpDev op, const Split sp, const StreamK sk) {
   using namespace tma;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
@@ -133,15 +152,28 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
   const int nN = (N + BN - 1) / BN;
   const int64_t tiles = ((M + BM - 1) / BM) * nN;
   const int KT = (K + BKS - 1) / BKS;
-  const int64_t my_tiles = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t total = my_tiles * KT;  // k-blocks this CTA consumes, over all its tiles
+  const int64_t S = gridDim.x, cta = blockIdx.x;
+  // whole tiles of this CTA, then its stream-K range [sk_b, sk_e) of k-blocks
+  // (SKT = false: the stream-K machinery is compiled out, whole tiles only)
+  const int64_t n_dp = SKT ? sk.dp_waves : (tiles > cta ? (tiles - 1 - cta) / S + 1 : 0);
+  const int64_t sk_b = SKT ? cta * sk.iters / S : 0, sk_e = SKT ? (cta + 1) * sk.iters / S : 0;
+  const int64_t total = n_dp * KT + (sk_e - sk_b);  // k-blocks this CTA consumes
+  auto sk_cta_of = [&](int64_t x) { return ((x + 1) * S + sk.iters - 1) / sk.iters - 1; };
 
-  // one lane issues the loads of k-block q (tile q / KT of this CTA)
+  // one lane issues the loads of this CTA's k-block q
   auto issue = [&](int64_t q) {
     const int s = static_cast<int>(q % TSTAGES);
     if (q >= TSTAGES) tma::mbar_wait(&empty[s], static_cast<unsigned>((q / TSTAGES - 1) & 1));
-    const int64_t tile = blockIdx.x + (q / KT) * gridDim.x;
-    const int kt = static_cast<int>(q % KT);
+    int64_t tile;
+    int kt;
+    if (!SKT || q < n_dp * KT) {
+      tile = cta + (q / KT) * S;
+      kt = static_cast<int>(q % KT);
+    } else {
+      const int64_t gi = sk_b + (q - n_dp * KT);
+      tile = sk.sk_base + gi / KT;
+      kt = static_cast<int>(gi % KT);
+    }
     const int n0 = static_cast<int>(tile % nN) * BN;
     const int64_t m0 = (tile / nN) * BM;
     unsigned char* st = smem + s * STAGE_BYTES;
@@ -186,7 +218,8 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
 
   const unsigned sbase = tma::su32(smem);
   int64_t q = 0;
-  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+  // k-blocks [k0, k1) of one tile, then its epilogue (or its stream-K piece)
+  auto run_tile = [&](const int64_t tile, const int k0, const int k1) {
     const int n0 = static_cast<int>(tile % nN) * BN;
     const int64_t m0 = (tile / nN) * BM;
     double cr[4][4][2], ci[4][4][2];
@@ -195,7 +228,7 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
 #pragma unroll
       for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
 
-    for (int kt = 0; kt < KT; ++kt, ++q) {
+    for (int kt = k0; kt < k1; ++kt, ++q) {
       if (leader && q + AHEAD < total) issue(q + AHEAD);
       const int s = static_cast<int>(q % TSTAGES);
       tma::mbar_wait(&full[s], static_cast<unsigned>((q / TSTAGES) & 1));
@@ -276,6 +309,60 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
       if (lane == 0) tma::mbar_arrive(&empty[s]);
     }
 
+    if (SKT && (k0 != 0 || k1 != KT)) {
+      // a piece of a stream-K tile: publish it, or (owner) add the later pieces in order
+      constexpr bool CO = CU || CL;
+      const int64_t tstart = (tile - sk.sk_base) * KT;
+      const int64_t owner = sk_cta_of(tstart);
+      auto slot = [&](int64_t piece) {
+        const int64_t idx = ((tile - sk.sk_base) * sk.slots + (piece - 1)) * CONSUMERS + warp;
+        return idx;
+      };
+      if (k0 != 0) {
+        const int64_t idx = slot(cta - owner);
+        double* dst = sk.part + idx * 2048;
+        int v = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              __stcg(dst + (v++) * 32 + lane, cr[i][j][h]);
+              if constexpr (CO) __stcg(dst + (v++) * 32 + lane, ci[i][j][h]);
+            }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(sk.flags + idx), "r"(sk.epoch) : "memory");
+        return;
+      }
+      const int64_t last = sk_cta_of(tstart + KT - 1);
+      for (int64_t piece = 1; piece <= last - owner; ++piece) {
+        const int64_t idx = slot(piece);
+        unsigned f = 0;
+        long long spins = 0;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(f) : "l"(sk.flags + idx) : "memory");
+          if (f != sk.epoch) {
+            __nanosleep(64);
+            if (++spins > (1ll << 28)) __trap();  // a lost partial must not hang the device
+          }
+        } while (f != sk.epoch);
+        const double* src = sk.part + idx * 2048;
+        int v = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              cr[i][j][h] += __ldcg(src + (v++) * 32 + lane);
+              if constexpr (CO) ci[i][j][h] += __ldcg(src + (v++) * 32 + lane);
+            }
+      }
+    }
+
     // epilogue (overlaps the producer's loads for the next tile)
     // fused ops run only where the host checked op_split_ok (inst_tma_c128.cu)
     const SplitOpCtx octx = split_ctx<OPK>(op);
@@ -319,6 +406,19 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
           dst[p] = narrow<TO>(re, im);
         }
       }
+    }
+  };
+
+  if constexpr (!SKT) {
+    for (int64_t tile = cta; tile < tiles; tile += S) run_tile(tile, 0, KT);
+  } else {
+    for (int64_t w = 0; w < n_dp; ++w) run_tile(cta + w * S, 0, KT);
+    for (int64_t gk = sk_b; gk < sk_e;) {
+      const int64_t tile = sk.sk_base + gk / KT;
+      const int k0 = static_cast<int>(gk % KT);
+      const int k1 = static_cast<int>(k0 + (sk_e - gk) < KT ? k0 + (sk_e - gk) : KT);
+      gk += k1 - k0;
+      run_tile(tile, k0, k1);
     }
   }
 }

@@ -1,0 +1,107 @@
+"""GPU: the stream-K tail of the TMA kernel (kmb200_tma.cuh, StreamK) against
+whole-tile scheduling (KM_POLICY_NO_STREAMK) and the oracle.
+
+Tile counts cover: fewer tiles than SMs (all stream-K), a partial last wave
+(whole waves + stream-K over the last two), exact multiples of the SM count
+(no stream-K), real and complex operands, the fused GPE epilogue, the
+blocked slab layouts, and repeated launches (per-launch epochs).
+"""
+
+import numpy as np
+import pytest
+
+import paper_2103_01691_b200 as km
+from oracle import kronmode_oracle as orc
+from paper_2103_01691_b200 import _device as dv
+from paper_2103_01691_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+
+def crand(rng, shape):
+    return np.asfortranarray(rng.standard_normal(shape) + 1j * rng.standard_normal(shape))
+
+
+def policies(fn):
+    """fn() with stream-K (AUTO), then with whole tiles only."""
+    lib = _native.lib()
+    try:
+        a = fn()
+        _native.check(lib.km_set_kernel_policy(_native.POLICY_NO_STREAMK))
+        b = fn()
+    finally:
+        _native.check(lib.km_set_kernel_policy(_native.POLICY_AUTO))
+    return a, b
+
+
+def dev(x):
+    import torch
+
+    return dv.to_device(x, x.dtype, torch.device("cuda", 0))
+
+
+# (shape, mu) with 128x64 tiles on 148 SMs: (1024, 1024) has 128 tiles (< 148: all stream-K);
+# 256^3 has 2048 = 13*148 + 124; the 256^2 x 32 slab has 256 = 148 + 108; (128, 64, 296)
+# along direction 2 has 296 = 2*148 (whole waves, no stream-K)
+CASES = [((1024, 1024), 1, False), ((1024, 1024), 2, False), ((1024, 1024), 1, True),
+         ((256, 256, 256), 1, True), ((256, 256, 256), 3, True), ((256, 256, 32), 3, True),
+         ((256, 256, 32), 1, True), ((256, 256, 64), 2, True), ((128, 64, 296), 2, True)]
+
+
+@pytest.mark.parametrize("shape,mu,cplx", CASES)
+def test_streamk_products(shape, mu, cplx):
+    rng = np.random.default_rng(sum(shape) + mu)
+    u = crand(rng, shape) if cplx else np.asfortranarray(rng.standard_normal(shape))
+    n = shape[mu - 1]
+    mat = rng.standard_normal((n, n)) + (1j * rng.standard_normal((n, n)) if cplx else 0)
+    t = dev(u)
+    a, b = policies(lambda: dv.to_host(km.mu_mode_product(t, mat, mu)))
+    want = orc.mu_mode_product(u, mat, mu)
+    assert orc.rel_l2(a, want) <= 1e-13
+    assert orc.rel_l2(b, want) <= 1e-13
+    assert orc.rel_l2(a, b) <= 1e-14
+
+
+def test_streamk_repeated_launches_are_deterministic():
+    rng = np.random.default_rng(7)
+    u = dev(crand(rng, (256, 256, 32)))
+    mat = rng.standard_normal((256, 256)) + 1j * rng.standard_normal((256, 256))
+    outs = [dv.to_host(km.mu_mode_product(u, mat, 1)).copy() for _ in range(5)]
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
+def test_streamk_step_and_gpe_epilogue():
+    n = 256
+    grids, lin_op, weights = km.gpe_setup(n)
+    from paper_2103_01691_b200.problems import weighted_vortex_state
+
+    psi = dev(weighted_vortex_state(grids, weights))
+    cache = km.prepare(lin_op, 0.1)
+    a, b = policies(lambda: dv.to_host(km.gpe_strang_step(cache, weights, psi, 0.1)))
+    want = orc.gpe_strang_step(cache.exps, weights, dv.to_host(psi), 0.1)
+    assert orc.rel_l2(a, want) <= 1e-12 and orc.rel_l2(b, want) <= 1e-12
+
+
+@pytest.mark.parametrize("P", [4, 8])
+def test_streamk_slab_layouts(P):
+    """The virtual-rank slab decomposition (blocked split layouts) with stream-K tails."""
+    import torch
+
+    from paper_2103_01691_b200 import dist
+
+    n = 256
+    rng = np.random.default_rng(P)
+    u = crand(rng, (n,) * 3)
+    d2 = km.heat_factors(n, 2).factors[0]
+    cache = km.prepare(km.KroneckerOp((1j * d2,) * 3), 0.01)
+
+    def run():
+        g = dist.VirtualSlabGroup(u, cache, torch.device("cuda", 0), P)
+        for _ in range(2):
+            g.step()
+        return g.gather()
+
+    a, b = policies(run)
+    want = orc.step(cache.exps, orc.step(cache.exps, u))
+    assert orc.rel_l2(a, want) <= 1e-12 and orc.rel_l2(b, want) <= 1e-12
