@@ -202,6 +202,46 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def e2e_slabs(runner, u_host, rank, world, dev, args):
+    """End-to-end at N > 1: every rank copies its input slab from pinned host memory, the ranks run
+    one distributed step (exchange included), and every rank copies its result slab back.
+    Not exercised with more than one GPU in round 1 (gpurun provides one).
+    Time = max over ranks of the host wall clock; bytes = the rank's slab each way."""
+    import torch
+    import torch.distributed as tdist
+
+    plan = runner.plan
+    slab = np.asfortranarray(plan.slab_a(u_host, rank))
+    h_in = torch.empty(plan.local, dtype=torch.complex128, pin_memory=True)
+    h_in.numpy()[...] = slab.reshape(-1, order="F")
+    h_out = torch.empty(plan.local, dtype=torch.complex128, pin_memory=True)
+
+    def one():
+        # fresh input each call, in the slab layout the schedule is in (A and B slabs have the same
+        # size; the layouts keep alternating, which the peer exchange's buffer parity relies on)
+        runner.a.copy_(h_in, non_blocking=True)
+        runner.step()
+        h_out.copy_(runner.a, non_blocking=True)
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        one()
+    steps = max(3, min(args.steps, 30))
+    tdist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    el = time.perf_counter() - t0
+    t = torch.tensor([el], device=dev, dtype=torch.float64)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    el = float(t.item())
+    nbytes = int(h_in.numel() * h_in.element_size())
+    return {"value": steps / el, "unit": "steps/s", "h2d_bytes_per_step": nbytes * world,
+            "d2h_bytes_per_step": nbytes * world, "steps": steps,
+            "call": "dist.SlabStepper: per-rank pinned slab -> device, one distributed step, slab -> pinned host"}
+
+
 def run_ours(args):
     import torch
 
@@ -264,6 +304,13 @@ def run_ours(args):
     if rank == 0:
         per_mode = runner.time_launches(reps=10) if world == 1 else None
         peak, peak_src = fp64_peak()
+        if world > 1:  # per-GPU share of the step's flops over the whole step (exchange included)
+            achieved = FLOP_PER_STEP / world / (ms_per_step * 1e-3) / 1e12
+            roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "kernel": "per-rank step: 3 x mumode_tma_kernel on the slab + exchange",
+                    "algorithmic_per_launch": f"{FLOP_PER_STEP // world} flop per rank per step",
+                    "peak_source": peak_src}
         if per_mode:
             flop_launch = 8 * N**4
             avg_ms = sum(per_mode) / len(per_mode)
@@ -294,6 +341,11 @@ def run_ours(args):
         e2e = {"value": e2e_steps / el, "unit": "steps/s", "h2d_bytes_per_step": int(host_in.nbytes),
                "d2h_bytes_per_step": int(out.nbytes), "steps": e2e_steps,
                "call": "paper_2103_01691_b200.step(cache, numpy F-array in pinned memory) -> numpy"}
+    else:
+        try:
+            e2e = e2e_slabs(runner, u_host, rank, world, dev, args)
+        except Exception as exc:  # an e2e failure must not lose the device-timed line
+            e2e = {"value": None, "unit": "steps/s", "error": f"{type(exc).__name__}: {exc}"}
 
     if rank == 0:
         cb = cpu_reference(u_host, cache, budget_s=20.0, max_steps=50) if (world == 1 and not args.no_cpu) else None
