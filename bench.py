@@ -261,8 +261,13 @@ def run_ours(args):
 
     u_host, cache = build_inputs()
     stream = torch.cuda.current_stream(dev)
+    slab = world > 1 or args.slab  # --slab: the multi-GPU code path on one rank (torchrun world 1)
+    if slab and world == 1:
+        import torch.distributed as tdist
 
-    if world == 1:
+        tdist.init_process_group("nccl", device_id=dev)
+
+    if not slab:
         state = dv.to_device(u_host, np.complex128, dev)
         mats = cache.device_exps((np.complex128,) * 3, dev)
         runner = dist.LocalStepper(state, mats)
@@ -302,9 +307,9 @@ def run_ours(args):
     # per-launch roofline of the dominant kernel (single GPU timing of one step's launches)
     roof = None
     if rank == 0:
-        per_mode = runner.time_launches(reps=10) if world == 1 else None
+        per_mode = runner.time_launches(reps=10) if not slab else None
         peak, peak_src = fp64_peak()
-        if world > 1:  # per-GPU share of the step's flops over the whole step (exchange included)
+        if slab:  # per-GPU share of the step's flops over the whole step (exchange included)
             achieved = FLOP_PER_STEP / world / (ms_per_step * 1e-3) / 1e12
             roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak, "traffic": None,
@@ -323,7 +328,7 @@ def run_ours(args):
 
     # e2e through the public drop-in call with host buffers
     e2e = None
-    if world == 1:
+    if not slab:
         pinned = torch.empty((N, N, N), dtype=torch.complex128, pin_memory=True)
         pinned_np = pinned.numpy()
         pinned_np[...] = u_host.transpose(2, 1, 0)  # C-order buffer ...
@@ -362,7 +367,7 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "complex128",
             "data": "synthetic (seeded normal complex tensor, host-built expm factors)",
-            "config": dict(WORKLOAD, parallelism=("single GPU" if world == 1 else
+            "config": dict(WORKLOAD, parallelism=("single GPU" if not slab else
                                                   f"slab{world} along direction 3, {args.exchange} exchange")),
             "gflops": value * FLOP_PER_STEP / 1e9,
             "roofline": roof,
@@ -372,7 +377,7 @@ def run_ours(args):
             "gpu_launches": runner.launches_per_step * args.steps,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if slab:
         import torch.distributed as tdist
 
         tdist.destroy_process_group()
@@ -385,6 +390,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--slab", action="store_true", help="run the multi-GPU slab path even on one rank (testing)")
     ap.add_argument("--exchange", choices=["nccl", "peer"], default="nccl",
                     help="multi-GPU all-to-all: NCCL, or fused into the products via NVLink peer stores")
     args = ap.parse_args()
