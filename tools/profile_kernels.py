@@ -64,6 +64,18 @@ def case_gpe():
     return lambda: km.gpe_strang_step(cache, weights, t, 0.1)
 
 
+def case_slab8():
+    """Rank 0's products of the 256^3 state split over 8 GPUs (stream-K tail), one step."""
+    from paper_2103_01691_b200 import dist
+
+    u = crand((256,) * 3)
+    d2 = km.heat_factors(256, 2).factors[0]
+    cache = km.prepare(km.KroneckerOp((1j * d2,) * 3), 0.01)
+    g = dist.VirtualSlabGroup(u, cache, DEV, 8)
+    r0 = g.ranks[0]
+    return lambda: (r0.pre_exchange(), r0.post_exchange())
+
+
 def case_norm():
     t = dv.to_device(crand((256,) * 3), np.complex128, DEV)
     w = [np.linspace(0.5, 1.5, 256)] * 3
@@ -71,7 +83,7 @@ def case_norm():
 
 
 CASES = {"c128": case_c128, "c64": case_c64, "small": case_small, "pipe": case_pipe, "gpe": case_gpe,
-         "norm": case_norm}
+         "norm": case_norm, "slab8": case_slab8}
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(CASES)
