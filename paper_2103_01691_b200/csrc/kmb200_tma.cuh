@@ -366,10 +366,10 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
     // epilogue (overlaps the producer's loads for the next tile)
     // fused ops run only where the host checked op_split_ok (inst_tma_c128.cu)
     const SplitOpCtx octx = split_ctx<OPK>(op);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    // one 8-row block of the warp tile: row i (runtime) with accumulators crow/cirow
+    auto emit_row = [&](const int i, const double (&crow)[4][2], const double (&cirow)[4][2]) {
       const int64_t f = m0 + wm + i * 8 + g;
-      if (f >= M) continue;
+      if (f >= M) return;
       const double lf = split_fiber_weight<OPK>(op, f);
       using TO = typename El<double, CU || CL>::T;
       const int64_t cs = KC ? 1 : nl;
@@ -399,12 +399,33 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
           const int col = c8 + 2 * t + h;
           if (col >= N) continue;
           const int64_t p = obj + static_cast<int64_t>(col) * cs;
-          double re = cr[i][j][h], im = (CU || CL) ? ci[i][j][h] : 0.0;
+          double re = crow[j][h], im = (CU || CL) ? cirow[j][h] : 0.0;
           if constexpr (OPK != KM_OP_NONE && (CU || CL)) {
             apply_op_fast<OPK>(op, octx, lf, col, re, im);
           }
           dst[p] = narrow<TO>(re, im);
         }
+      }
+    };
+    if constexpr (OPK == KM_OP_NONE) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) emit_row(i, cr[i], ci[i]);
+    } else {
+      // the phase math is ~80 instructions per element: emit the rows in a
+      // rolled loop that rotates row i+1 into row 0, so the code holds 8 copies
+      // of it instead of 32 (the unrolled version stalled on instruction fetch)
+#pragma unroll 1
+      for (int i = 0; i < 4; ++i) {
+        emit_row(i, cr[0], ci[0]);
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              cr[r][j][h] = cr[r + 1][j][h];
+              ci[r][j][h] = ci[r + 1][j][h];
+            }
       }
     }
   };
