@@ -37,11 +37,15 @@
 
 namespace kmb {
 
+#ifndef KMB_TMA_AHEAD
+#define KMB_TMA_AHEAD 2
+#endif
+
 namespace tma {
 
 constexpr int BM = 128, BN = 64, BKS = 16, TSTAGES = 4, CONSUMERS = 8;
 constexpr int THREADS = 32 * CONSUMERS;
-constexpr int AHEAD = 2;  // k-blocks between a stage's load and its use
+constexpr int AHEAD = KMB_TMA_AHEAD;  // k-blocks between a stage's load and its use
 constexpr int A_BYTES = BM * BKS * 16, B_BYTES = BN * BKS * 16, STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int SMEM_BYTES = TSTAGES * STAGE_BYTES + 2 * TSTAGES * 8 + 1024;
 
