@@ -105,3 +105,22 @@ def test_streamk_slab_layouts(P):
     a, b = policies(run)
     want = orc.step(cache.exps, orc.step(cache.exps, u))
     assert orc.rel_l2(a, want) <= 1e-12 and orc.rel_l2(b, want) <= 1e-12
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_large_shapes_vs_oracle(seed):
+    """Ragged shapes large enough for the persistent TMA kernel (and, where the tile count
+    lands between one and four waves, its stream-K tail): every direction, against the oracle."""
+    rng = np.random.default_rng(100 + seed)
+    n1 = int(rng.choice([128, 256]))  # fiber-contiguous layouts need n_left % 128 == 0
+    shape = (n1, int(rng.integers(40, 300)) // 8 * 8, int(rng.integers(40, 200)) // 8 * 8)
+    u = crand(rng, shape)
+    t = dev(u)
+    for mu in (1, 2, 3):
+        n = shape[mu - 1]
+        m = int(rng.integers(n // 2, n + 40))
+        mat = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
+        a, b = policies(lambda: dv.to_host(km.mu_mode_product(t, mat, mu)))
+        want = orc.mu_mode_product(u, mat, mu)
+        assert orc.rel_l2(a, want) <= 1e-13, (shape, mu, m)
+        assert orc.rel_l2(b, want) <= 1e-13, (shape, mu, m)
