@@ -1,5 +1,5 @@
 // Host side of the tcgen05 complex64 μ-mode product: factor planes, TMA maps, launch.
-#include "kmb200_tc32.cuh"
+#include "kmb200_tc32k.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -31,27 +31,20 @@ bool map_f32(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool KC>
-int launch(const CUtensorMap& ahi, const CUtensorMap& alo, const CUtensorMap& b, const CUtensorMap& mo, int64_t F,
-           int m, int K, int64_t nl, cudaStream_t st) {
-  auto kern = mumode_tc32_kernel<KC>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tc32::SMEM_BYTES);
-    if (e != cudaSuccess) return fail(KM_ECUDA, "cudaFuncSetAttribute(tc32): %s", cudaGetErrorString(e));
-    attr = true;
-  }
-  const int64_t fib_r = KC ? F : 2 * F;
-  // CTA pairs (cluster of 2): one pair per 256 E rows x 256 tensor columns
-  const int64_t tiles = ((2 * m + 2 * tc32::BMR - 1) / (2 * tc32::BMR)) * ((fib_r + tc32::BNR - 1) / tc32::BNR);
-  // not every SM can host half of a pair (TPCs with one usable SM): size the
-  // persistent grid by the clusters that are co-resident
-  static int max_pairs = 0;
+// Persistent launch of a CTA-pair kernel: one pair per (2*BMR) E rows x BNR
+// tensor columns, the grid sized by the clusters that can be co-resident
+// (not every SM can host half of a pair: TPCs with one usable SM).
+template <typename Kern>
+int launch_pairs(Kern kern, int smem, int threads, int64_t tiles, const char* what, const CUtensorMap& ahi,
+                 const CUtensorMap& alo, const CUtensorMap& b, const CUtensorMap& mo, int64_t F, int m, int K,
+                 int64_t nl, cudaStream_t st, int& max_pairs) {
   if (max_pairs == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return fail(KM_ECUDA, "cudaFuncSetAttribute(%s): %s", what, cudaGetErrorString(e));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * (num_sms() / 2));
-    cfg.blockDim = dim3(tc32::THREADS);
-    cfg.dynamicSmemBytes = tc32::SMEM_BYTES;
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute attr_c;
     attr_c.id = cudaLaunchAttributeClusterDimension;
     attr_c.val.clusterDim.x = 2;
@@ -64,8 +57,24 @@ int launch(const CUtensorMap& ahi, const CUtensorMap& alo, const CUtensorMap& b,
     max_pairs = n;
   }
   const int64_t pairs = tiles < max_pairs ? tiles : max_pairs;
-  kern<<<static_cast<unsigned>(2 * pairs), tc32::THREADS, tc32::SMEM_BYTES, st>>>(ahi, alo, b, mo, F, m, K, nl);
-  return check_launch("mumode_tc32_kernel");
+  kern<<<static_cast<unsigned>(2 * pairs), threads, smem, st>>>(ahi, alo, b, mo, F, m, K, nl);
+  return check_launch(what);
+}
+
+template <bool KC>
+int launch(const CUtensorMap& ahi, const CUtensorMap& alo, const CUtensorMap& b, const CUtensorMap& mo, int64_t F,
+           int m, int K, int64_t nl, bool chunked, cudaStream_t st) {
+  const int64_t fib_r = KC ? F : 2 * F;
+  if (chunked) {
+    static int max_pairs = 0;
+    const int64_t tiles = ((2 * m + 2 * tc32k::BMR - 1) / (2 * tc32k::BMR)) * ((fib_r + tc32k::BNR - 1) / tc32k::BNR);
+    return launch_pairs(mumode_tc32_chunk_kernel<KC>, tc32k::SMEM_BYTES, tc32k::THREADS, tiles,
+                        "mumode_tc32_chunk_kernel", ahi, alo, b, mo, F, m, K, nl, st, max_pairs);
+  }
+  static int max_pairs = 0;
+  const int64_t tiles = ((2 * m + 2 * tc32::BMR - 1) / (2 * tc32::BMR)) * ((fib_r + tc32::BNR - 1) / tc32::BNR);
+  return launch_pairs(mumode_tc32_kernel<KC>, tc32::SMEM_BYTES, tc32::THREADS, tiles, "mumode_tc32_kernel", ahi,
+                      alo, b, mo, F, m, K, nl, st, max_pairs);
 }
 
 }  // namespace
@@ -81,8 +90,11 @@ int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t 
   if ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(ws)) & 15) return -1;
   if (K % 4 != 0 || m % 2 != 0 || m > (1 << 20) || K > (1 << 20)) return -1;
   if (reinterpret_cast<uintptr_t>(out) & 15) return -1;
-  if (!kc && nl % (tc32::BNR / 2) != 0) return -1;  // a tile's fibers lie inside one slab
-  if ((kc ? 2 * K : K) > 512) return -1;  // accumulation error grows with K' (see kmb200_tc32.cuh)
+  // K' <= 512: one accumulation chain per tile (kmb200_tc32.cuh); longer
+  // contractions use the chunked kernel, whose chains stay at 64 k' (kmb200_tc32k.cuh)
+  const bool chunked = (kc ? 2 * K : K) > 512;
+  const int64_t tile_fibers = (chunked ? tc32k::BNR : tc32::BNR) / 2;
+  if (!kc && nl % tile_fibers != 0) return -1;  // a pair tile's fibers lie inside one slab
   if (F >= (int64_t(1) << 31)) return -1;
   float* planes = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
   {
@@ -110,7 +122,8 @@ int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t 
   if (kc) {
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(2 * K), static_cast<cuuint64_t>(F), 1};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(2 * K) * 4, static_cast<cuuint64_t>(2 * K) * 4 * F};
-    cuuint32_t box[3] = {tc32::BKR, tc32::BNH, 1};  // each CTA of the pair stages half of the tile's columns
+    const cuuint32_t bnh = chunked ? tc32k::BNH : tc32::BNH;  // each CTA of the pair stages half the columns
+    cuuint32_t box[3] = {tc32::BKR, bnh, 1};
     if (!map_f32(&mb, u, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B)) return -1;
     // output (F x m complex, row-major in n): boxes of 32 fibers x 16 complex n
     CUtensorMap mo;
@@ -118,13 +131,13 @@ int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t 
     cuuint64_t os[2] = {static_cast<cuuint64_t>(2 * m) * 4, static_cast<cuuint64_t>(2 * m) * 4 * F};
     cuuint32_t ob[3] = {32, 32, 1};
     if (!map_f32(&mo, out, 3, od, os, ob)) return -1;
-    return launch<true>(mahi, malo, mb, mo, F, static_cast<int>(m), static_cast<int>(K), nl, st);
+    return launch<true>(mahi, malo, mb, mo, F, static_cast<int>(m), static_cast<int>(K), nl, chunked, st);
   }
   cuuint64_t dims[5] = {32, static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(nl / 16), static_cast<cuuint64_t>(nr),
                         1};
   cuuint64_t strides[4] = {static_cast<cuuint64_t>(nl) * 8, 128, static_cast<cuuint64_t>(nl) * K * 8,
                            static_cast<cuuint64_t>(nl) * K * 8 * nr};
-  cuuint32_t box[5] = {32, tc32::BKR, tc32::BNH / 32, 1, 1};
+  cuuint32_t box[5] = {32, tc32::BKR, static_cast<cuuint32_t>((chunked ? tc32k::BNH : tc32::BNH) / 32), 1, 1};
   // MN-major tf32 operand: 32-B swizzle atoms (matches the BASE32B descriptor layout)
   if (!map_f32(&mb, u, 5, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return -1;
   // output (n_left x m x n_right complex): boxes of 16 fibers x 16 rows n
@@ -133,7 +146,7 @@ int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t 
   cuuint64_t os[2] = {static_cast<cuuint64_t>(nl) * 8, static_cast<cuuint64_t>(nl) * m * 8};
   cuuint32_t ob[3] = {32, 16, 1};
   if (!map_f32(&mo, out, 3, od, os, ob)) return -1;
-  return launch<false>(mahi, malo, mb, mo, F, static_cast<int>(m), static_cast<int>(K), nl, st);
+  return launch<false>(mahi, malo, mb, mo, F, static_cast<int>(m), static_cast<int>(K), nl, chunked, st);
 }
 
 }  // namespace kmb

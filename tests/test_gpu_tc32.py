@@ -54,11 +54,18 @@ def test_c64_step_256_vs_oracle_and_dmma():
     assert orc.rel_l2(got, dmma) <= 1e-5
 
 
-def test_long_contraction_stays_on_dmma_and_accurate():
-    # K' = 2*n_mu > 512 for direction 1: the host keeps it on the DMMA path
-    rng = np.random.default_rng(9)
-    u = crand(rng, (384, 64, 8))
-    mat = ((rng.standard_normal((384, 384)) + 1j * rng.standard_normal((384, 384))) / 20).astype(np.complex64)
-    got = km.mu_mode_product(u, mat, 1)
-    want128 = orc.mu_mode_product(u.astype(np.complex128), mat.astype(np.complex128), 1)
-    assert orc.rel_l2(got, want128) <= 1e-6
+@pytest.mark.parametrize("shape,mu", [((384, 64, 8), 1), ((512, 128, 8), 1), ((1024, 64, 4), 1),
+                                      ((128, 1024, 8), 2), ((128, 8, 1024), 3), ((256, 8, 640), 3)])
+def test_long_contractions_chunked_accumulation(shape, mu):
+    """K' > 512: the chunked tcgen05 kernel (fresh TMEM accumulator every 64 k', fp32 drain) keeps
+    the error at the short-contraction level instead of growing with K."""
+    rng = np.random.default_rng(sum(shape) + mu)
+    u = crand(rng, shape)
+    n = shape[mu - 1]
+    mat = ((rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(n)).astype(np.complex64)
+    got = km.mu_mode_product(u, mat, mu)
+    want128 = orc.mu_mode_product(u.astype(np.complex128), mat.astype(np.complex128), mu)
+    want64 = orc.mu_mode_product(u, mat, mu)
+    e128, e64 = orc.rel_l2(got, want128), orc.rel_l2(got, want64)
+    assert e128 <= 2e-6, e128
+    assert e64 <= 1e-5, e64
