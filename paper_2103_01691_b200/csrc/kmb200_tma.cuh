@@ -371,10 +371,11 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
     // fused ops run only where the host checked op_split_ok (inst_tma_c128.cu)
     const SplitOpCtx octx = split_ctx<OPK>(op);
     // one 8-row block of the warp tile: row i (runtime) with accumulators crow/cirow
-    auto emit_row = [&](const int i, const double (&crow)[4][2], const double (&cirow)[4][2]) {
+    // (with_op false: the values were already transformed, gpe_rows below)
+    auto emit_row = [&](const int i, const double (&crow)[4][2], const double (&cirow)[4][2], const bool with_op) {
       const int64_t f = m0 + wm + i * 8 + g;
       if (f >= M) return;
-      const double lf = split_fiber_weight<OPK>(op, f);
+      const double lf = with_op ? split_fiber_weight<OPK>(op, f) : 0.0;
       using TO = typename El<double, CU || CL>::T;
       const int64_t cs = KC ? 1 : nl;
       TO* obase = out;
@@ -405,7 +406,7 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
           const int64_t p = obj + static_cast<int64_t>(col) * cs;
           double re = crow[j][h], im = (CU || CL) ? cirow[j][h] : 0.0;
           if constexpr (OPK != KM_OP_NONE && (CU || CL)) {
-            apply_op_fast<OPK>(op, octx, lf, col, re, im);
+            if (with_op) apply_op_fast<OPK>(op, octx, lf, col, re, im);
           }
           dst[p] = narrow<TO>(re, im);
         }
@@ -413,14 +414,57 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
     };
     if constexpr (OPK == KM_OP_NONE) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) emit_row(i, cr[i], ci[i]);
+      for (int i = 0; i < 4; ++i) emit_row(i, cr[i], ci[i], false);
+    } else if constexpr (OPK == KM_OP_GPE_PHASE && (CU || CL)) {
+      // GPE phase: the thread's 8 columns are fixed for the tile, so their
+      // direction-d weights are loaded once; each 8-element row is rotated
+      // as one vector (gpe_rotate_vec: 8 independent chains, one warp vote
+      // for the reduction-free sin/cos).  Every lane takes part (out-of-range
+      // elements compute on zeros and are not stored).
+      double wl[4][2];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = n0 + wn + j * 8 + 2 * t + h;
+          wl[j][h] = col < N ? __ldg(octx.wlast + col) : 1.0;
+        }
+#pragma unroll 1
+      for (int i = 0; i < 4; ++i) {
+        const int64_t f = m0 + wm + i * 8 + g;
+        const double lf = f < M ? split_fiber_weight<OPK>(op, f) : 1.0;
+        double w[8], vr[8], vi[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          w[e] = __dmul_rn(lf, wl[e >> 1][e & 1]);
+          vr[e] = cr[0][e >> 1][e & 1];
+          vi[e] = ci[0][e >> 1][e & 1];
+        }
+        gpe_rotate_vec<8>(op.coef, w, vr, vi);
+        if (op.repeat > 1) gpe_rotate_vec<8>(op.coef, w, vr, vi);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          cr[0][e >> 1][e & 1] = vr[e];
+          ci[0][e >> 1][e & 1] = vi[e];
+        }
+        emit_row(i, cr[0], ci[0], false);
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              cr[r][j][h] = cr[r + 1][j][h];
+              ci[r][j][h] = ci[r + 1][j][h];
+            }
+      }
     } else {
       // the phase math is ~80 instructions per element: emit the rows in a
       // rolled loop that rotates row i+1 into row 0, so the code holds 8 copies
       // of it instead of 32 (the unrolled version stalled on instruction fetch)
 #pragma unroll 1
       for (int i = 0; i < 4; ++i) {
-        emit_row(i, cr[0], ci[0]);
+        emit_row(i, cr[0], ci[0], true);
 #pragma unroll
         for (int r = 0; r < 3; ++r)
 #pragma unroll
