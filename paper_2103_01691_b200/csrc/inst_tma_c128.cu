@@ -71,34 +71,39 @@ int set_smem(Kern k) {
   return e == cudaSuccess ? KM_OK : fail(KM_ECUDA, "cudaFuncSetAttribute(tma): %s", cudaGetErrorString(e));
 }
 
-// Stream-K launch of a complex x complex product.  Returns -1 when the shape or
-// the stream does not call for it (the caller launches whole tiles).
+// Stream-K launch of a product (any real / complex mix).  Returns -1 when the
+// shape or the stream does not call for it (the caller launches whole tiles).
 // Stream-K pays for products whose tiles make 1-4 waves with a partial last
 // one (e.g. the 256^3 state split over 4 or 8 GPUs): that wave plus one full
 // wave is cut into equal k-ranges, so every CTA's range holds at least KT
 // k-blocks.  Measured (tools/slab_probe.py): per-rank products at P = 4 / 8 go
-// from 0.80 / 0.78 to 0.88 / 0.83 of the DMMA peak.  Fewer tiles than SMs (the
-// 1024^2 real pipe-flow product) and many-wave launches measured no gain.
-template <bool KC, int OPK>
-int launch_streamk(const CUtensorMap& ma, const CUtensorMap& mb, double2* out, int64_t M, int N, int K, int64_t nl,
+// from 0.80 / 0.78 to 0.88 / 0.83 of the DMMA peak.  Between S/2 and S tiles
+// all k-blocks are cut into S ranges (tools/pipe_probe.py: the 1024^2 f64
+// pipe-flow step 189 -> 176 us, its complex128 variant 296 -> 283 us).
+// Many-wave launches measured no gain (1.2 % tail at 256^3).
+template <bool KC, int OPK, bool CL, bool CU>
+int launch_streamk(const CUtensorMap& ma, const CUtensorMap& mb, void* out, int64_t M, int N, int K, int64_t nl,
                    const OpDev& op, const Split& sp, cudaStream_t st) {
+  using TO = typename El<double, CU || CL>::T;
   const int64_t tiles = ((M + tma::BM - 1) / tma::BM) * ((N + tma::BN - 1) / tma::BN);
   const int64_t KT = (K + tma::BKS - 1) / tma::BKS;
   const int64_t S = num_sms();
-  if (g_streamk_disabled || tiles <= S || tiles % S == 0 || tiles > 4 * S || KT < 2) return -1;
+  // fewer tiles than SMs (down to S/2): every k-block goes to the stream-K
+  // range, a tile spans at most 3 CTAs (slots <= 2)
+  if (g_streamk_disabled || 2 * tiles < S || tiles % S == 0 || tiles > 4 * S || KT < 2) return -1;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(st, &cap);
   if (cap != cudaStreamCaptureStatusNone) return -1;  // epochs would repeat on replay
   StreamK sk;
   memset(&sk, 0, sizeof(sk));
-  sk.dp_waves = tiles / S - 1;
+  sk.dp_waves = tiles > S ? tiles / S - 1 : 0;
   sk.sk_base = sk.dp_waves * S;
   sk.iters = (tiles - sk.sk_base) * KT;
-  const int64_t per = sk.iters / S;                      // >= KT: a tile spans at most 2 CTAs
+  const int64_t per = sk.iters / S;  // >= KT (tiles > S: a tile spans at most 2 CTAs) or >= KT/2
   sk.slots = static_cast<int>((KT + per - 1) / per);
   SkScratch* scr = sk_scratch(st);
   if (!scr) return -1;
-  auto kern = mumode_tma_kernel<KC, OPK, true, true, true>;
+  auto kern = mumode_tma_kernel<KC, OPK, CL, CU, true>;
   static bool attr = false;
   if (!attr) {
     if (int rc = set_smem(kern)) return rc;
@@ -107,7 +112,8 @@ int launch_streamk(const CUtensorMap& ma, const CUtensorMap& mb, double2* out, i
   sk.part = scr->part;
   sk.flags = scr->flags;
   sk.epoch = ++scr->epoch;
-  void* args[] = {const_cast<CUtensorMap*>(&ma), const_cast<CUtensorMap*>(&mb), &out, &M, &N, &K, &nl,
+  TO* outp = static_cast<TO*>(out);
+  void* args[] = {const_cast<CUtensorMap*>(&ma), const_cast<CUtensorMap*>(&mb), &outp, &M, &N, &K, &nl,
                   const_cast<OpDev*>(&op), const_cast<Split*>(&sp), &sk};
   cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(static_cast<unsigned>(S)),
                                               dim3(tma::THREADS), args, tma::SMEM_BYTES, st);
@@ -118,8 +124,8 @@ template <bool KC, int OPK, bool CL, bool CU>
 int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* out, int64_t M, int N, int K, int64_t nl,
            const OpDev& op, const Split& sp, cudaStream_t st) {
   using TO = typename El<double, CU || CL>::T;
-  if constexpr (CU && CL) {
-    const int rc = launch_streamk<KC, OPK>(ma, mb, static_cast<double2*>(out), M, N, K, nl, op, sp, st);
+  {
+    const int rc = launch_streamk<KC, OPK, CL, CU>(ma, mb, out, M, N, K, nl, op, sp, st);
     if (rc >= 0) return rc;
   }
   auto kern = mumode_tma_kernel<KC, OPK, CL, CU, false>;
