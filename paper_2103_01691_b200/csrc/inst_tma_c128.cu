@@ -139,7 +139,9 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* out, int64_t M, i
   StreamK none;
   memset(&none, 0, sizeof(none));
   const int grid = static_cast<int>(tiles < S ? tiles : S);
-  kern<<<grid, tma::THREADS, tma::SMEM_BYTES, st>>>(ma, mb, static_cast<TO*>(out), M, N, K, nl, op, sp, none);
+  const cudaError_t e = launch_pdl(kern, dim3(grid), dim3(tma::THREADS), tma::SMEM_BYTES, st, ma, mb,
+                                   static_cast<TO*>(out), M, N, K, nl, op, sp, none);
+  if (e != cudaSuccess) return fail(KM_ECUDA, "mumode_tma_kernel: %s", cudaGetErrorString(e));
   return check_launch("mumode_tma_kernel");
 }
 

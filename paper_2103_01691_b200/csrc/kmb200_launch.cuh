@@ -23,8 +23,10 @@ int launch_cfg(const void* u, const void* L, void* out, int64_t M, int N, int K,
   }
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   if (tiles > 0x7fffffffLL) return fail(KM_EINVAL, "km_mumode: %lld tiles exceed the grid limit", (long long)tiles);
-  kern<<<static_cast<unsigned>(tiles), 32 * WM_ * WN_, Lay::TOTAL, st>>>(
-      static_cast<const TU*>(u), static_cast<const TL*>(L), static_cast<TO*>(out), M, N, K, nl, op, sp);
+  const cudaError_t e = launch_pdl(kern, dim3(static_cast<unsigned>(tiles)), dim3(32 * WM_ * WN_), Lay::TOTAL, st,
+                                   static_cast<const TU*>(u), static_cast<const TL*>(L), static_cast<TO*>(out), M, N,
+                                   K, nl, op, sp);
+  if (e != cudaSuccess) return fail(KM_ECUDA, "mumode_kernel: %s", cudaGetErrorString(e));
   return check_launch("mumode_kernel");
 }
 

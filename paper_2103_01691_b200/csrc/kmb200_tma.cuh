@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
     tma::fence_barrier_init();
   }
   __syncthreads();
+  pdl_wait();  // the previous product's output is this one's input
 
   const int nN = (N + BN - 1) / BN;
   const int64_t tiles = ((M + BM - 1) / BM) * nN;

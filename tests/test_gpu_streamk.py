@@ -62,6 +62,27 @@ def test_streamk_products(shape, mu, cplx):
     assert orc.rel_l2(a, b) <= 1e-14
 
 
+# real x complex mixes (Hermite transforms, complex pipe-flow variant) and a
+# tile count where a tile spans three CTAs: (1024, 896) along direction 2 has
+# 8 x 14 = 112 tiles (S/2 <= 112 < S), 112 * 64 / 148 = 48 k-blocks per CTA
+MIX_CASES = [((1024, 1024), 1, "rc"), ((1024, 1024), 2, "rc"), ((1024, 1024), 2, "cr"),
+             ((1024, 896), 2, "rr"), ((1024, 896), 2, "cc"), ((896, 1024), 1, "rc")]
+
+
+@pytest.mark.parametrize("shape,mu,mix", MIX_CASES)
+def test_streamk_mixed_dtypes(shape, mu, mix):
+    rng = np.random.default_rng(sum(shape) + mu + len(mix))
+    u = crand(rng, shape) if mix[0] == "c" else np.asfortranarray(rng.standard_normal(shape))
+    n = shape[mu - 1]
+    mat = rng.standard_normal((n, n)) + (1j * rng.standard_normal((n, n)) if mix[1] == "c" else 0)
+    t = dev(u)
+    a, b = policies(lambda: dv.to_host(km.mu_mode_product(t, mat, mu)))
+    want = orc.mu_mode_product(u, mat, mu)
+    assert orc.rel_l2(a, want) <= 1e-13
+    assert orc.rel_l2(b, want) <= 1e-13
+    assert orc.rel_l2(a, b) <= 1e-14
+
+
 def test_streamk_repeated_launches_are_deterministic():
     rng = np.random.default_rng(7)
     u = dev(crand(rng, (256, 256, 32)))
