@@ -253,18 +253,44 @@ def to_host(t):
 _VEC_CACHE = {}
 _VEC_CACHE_MAX = 64
 
+try:
+    _libc_memcmp = ctypes.CDLL(None).memcmp
+    _libc_memcmp.restype = ctypes.c_int
+    _libc_memcmp.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]
+except (OSError, AttributeError):  # pragma: no cover - every Linux libc has memcmp
+    _libc_memcmp = None
+
+
+def _same_bytes(a, b):
+    """Byte equality of two arrays with the same dtype, shape and memory order."""
+    if a.nbytes == 0:
+        return True
+    if _libc_memcmp is not None:
+        return _libc_memcmp(a.ctypes.data, b.ctypes.data, a.nbytes) == 0
+    return np.array_equal(a.reshape(-1, order="K").view(np.uint8), b.reshape(-1, order="K").view(np.uint8))
+
 
 def cached_vector(v, dtype, dev):
-    """Device copy of a small host vector/matrix, memoised by content."""
+    """Device copy of a small host vector/matrix, memoised per host buffer.
+
+    The entry is keyed by the host buffer (address, dtype, shape, strides) and
+    validated on every hit with a memcmp against a snapshot taken at upload, so
+    an array modified in place (or a new array at a recycled address) is
+    uploaded again.  A memcmp reads the matrix once; hashing its bytes, the
+    previous key, cost ~6x more host time per call (1 ms for a 512 x 512
+    complex64 factor, on the critical path of every mu_mode_product call).
+    """
     if is_tensor(v):
         return v.to(device=dev, dtype=torch_dtype(dtype)).contiguous()
-    arr = np.ascontiguousarray(np.asarray(v), dtype=dtype)
-    key = (str(dev), arr.dtype.str, arr.shape, arr.tobytes())
+    src = np.asarray(v)
+    if not (src.flags.c_contiguous or src.flags.f_contiguous):
+        src = np.ascontiguousarray(src)
+    key = (str(dev), np.dtype(dtype).str, src.dtype.str, src.shape, src.strides, src.ctypes.data)
     hit = _VEC_CACHE.get(key)
-    if hit is not None:
-        return hit
-    t = upload(arr, dev)
-    if len(_VEC_CACHE) >= _VEC_CACHE_MAX:
+    if hit is not None and _same_bytes(hit[0], src):
+        return hit[1]
+    t = upload(np.ascontiguousarray(src, dtype=dtype), dev)
+    if hit is None and len(_VEC_CACHE) >= _VEC_CACHE_MAX:
         _VEC_CACHE.pop(next(iter(_VEC_CACHE)))
-    _VEC_CACHE[key] = t
+    _VEC_CACHE[key] = (src.copy(order="K"), t)
     return t

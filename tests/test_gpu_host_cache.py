@@ -1,0 +1,49 @@
+"""GPU: the device copies of host factors (_device.cached_vector) follow the
+host arrays: an in-place change, a recycled buffer or a different dtype view
+is uploaded again, so mu_mode_product always sees the current values (the
+reference multiplies by the array as it is at call time, tensor.py:129/139)."""
+
+import numpy as np
+import pytest
+
+import paper_2103_01691_b200 as km
+from oracle import kronmode_oracle as orc
+from paper_2103_01691_b200 import _device as dv
+
+pytestmark = pytest.mark.gpu
+
+
+def test_in_place_change_of_a_factor_is_seen():
+    rng = np.random.default_rng(3)
+    u = np.asfortranarray(rng.standard_normal((16, 12, 8)) + 1j * rng.standard_normal((16, 12, 8)))
+    mat = rng.standard_normal((12, 12)) + 1j * rng.standard_normal((12, 12))
+    for mu_val in range(3):
+        got = km.mu_mode_product(u, mat, 2)
+        assert orc.rel_l2(got, orc.mu_mode_product(u, mat, 2)) <= 1e-14
+        mat[mu_val, 5] += 1.0  # same buffer, new content
+        mat[7, :] *= -0.5
+
+
+def test_fortran_and_c_order_factors_and_weights():
+    rng = np.random.default_rng(4)
+    u = np.asfortranarray(rng.standard_normal((8, 8, 8)))
+    mat = rng.standard_normal((8, 8))
+    for m in (mat, np.asfortranarray(mat), mat.T, mat[:, ::-1]):
+        got = km.mu_mode_product(u, m, 3)
+        assert orc.rel_l2(got, orc.mu_mode_product(u, m, 3)) <= 1e-14
+
+
+def test_cache_hit_returns_the_same_device_copy():
+    import torch
+
+    dev = torch.device("cuda", 0)
+    a = np.arange(64.0).reshape(8, 8)
+    t1 = dv.cached_vector(a, np.float64, dev)
+    t2 = dv.cached_vector(a, np.float64, dev)
+    assert t1 is t2
+    a[0, 0] = -1.0
+    t3 = dv.cached_vector(a, np.float64, dev)
+    assert t3 is not t1 and float(t3[0, 0]) == -1.0
+    # same buffer, another target dtype: a separate entry
+    t4 = dv.cached_vector(a, np.float32, dev)
+    assert t4.dtype == torch.float32 and float(t4[0, 0]) == -1.0
