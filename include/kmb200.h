@@ -80,7 +80,12 @@ typedef struct km_pointop {
  * (~76 MB on 148 SMs).  Launches captured into a CUDA graph keep whole tiles:
  * the partials' publish flags are per-launch epochs, which a replayed graph
  * would repeat. */
-enum km_kernel_policy { KM_POLICY_AUTO = 0, KM_POLICY_NO_TMA = 1, KM_POLICY_NO_STREAMK = 2 };
+enum km_kernel_policy {
+  KM_POLICY_AUTO = 0,
+  KM_POLICY_NO_TMA = 1,
+  KM_POLICY_NO_STREAMK = 2,
+  KM_POLICY_NO_TC_HALVES = 4  /* complex64 K' in (512, 1024] on the chunked tcgen05 kernel */
+};
 int km_set_kernel_policy(int policy);
 
 /* ABI version and build info */

@@ -22,7 +22,7 @@ MAX_D = 8
 KM_F32, KM_F64, KM_C64, KM_C128 = 0, 1, 2, 3
 KM_OK, KM_EINVAL, KM_ECUDA = 0, 1, 2
 OP_NONE, OP_GPE_PHASE, OP_DIAG = 0, 1, 2
-POLICY_AUTO, POLICY_NO_TMA, POLICY_NO_STREAMK = 0, 1, 2
+POLICY_AUTO, POLICY_NO_TMA, POLICY_NO_STREAMK, POLICY_NO_TC_HALVES = 0, 1, 2, 4
 
 # every symbol include/kmb200.h declares
 EXPORTS = (

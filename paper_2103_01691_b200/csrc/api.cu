@@ -11,6 +11,7 @@ namespace kmb {
 
 extern bool g_tma_disabled;     // inst_tma_c128.cu
 extern bool g_streamk_disabled;  // inst_tma_c128.cu
+extern bool g_tc_halves_disabled;  // inst_tc32_c64.cu
 size_t tc32_workspace_bytes(int64_t m, int64_t K);  // inst_tc32_c64.cu
 int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t nl, int64_t K, int64_t nr, void* ws,
                     size_t ws_bytes, cudaStream_t st);
@@ -238,10 +239,11 @@ extern "C" {
 int km_abi_version(void) { return KMB200_ABI_VERSION; }
 
 int km_set_kernel_policy(int policy) {
-  if (policy < 0 || policy > (KM_POLICY_NO_TMA | KM_POLICY_NO_STREAMK))
+  if (policy < 0 || policy > (KM_POLICY_NO_TMA | KM_POLICY_NO_STREAMK | KM_POLICY_NO_TC_HALVES))
     return fail(KM_EINVAL, "km_set_kernel_policy: unknown policy %d", policy);
   g_tma_disabled = (policy & KM_POLICY_NO_TMA) != 0;
   g_streamk_disabled = (policy & KM_POLICY_NO_STREAMK) != 0;
+  g_tc_halves_disabled = (policy & KM_POLICY_NO_TC_HALVES) != 0;
   return KM_OK;
 }
 

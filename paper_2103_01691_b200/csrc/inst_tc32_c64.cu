@@ -5,6 +5,8 @@
 
 namespace kmb {
 
+bool g_tc_halves_disabled = false;  // A/B switch (KMB200_TC_HALVES=0): K' in (512, 1024] on the chunked kernel
+
 namespace {
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn32() {
@@ -71,8 +73,13 @@ int launch(const CUtensorMap& ahi, const CUtensorMap& alo, const CUtensorMap& b,
     return launch_pairs(mumode_tc32_chunk_kernel<KC>, tc32k::SMEM_BYTES, tc32k::THREADS, tiles,
                         "mumode_tc32_chunk_kernel", ahi, alo, b, mo, F, m, K, nl, st, max_pairs);
   }
-  static int max_pairs = 0;
   const int64_t tiles = ((2 * m + 2 * tc32::BMR - 1) / (2 * tc32::BMR)) * ((fib_r + tc32::BNR - 1) / tc32::BNR);
+  if ((KC ? 2 * K : K) > 512) {  // two accumulation chains of <= 512 k' per tile
+    static int max_pairs = 0;
+    return launch_pairs(mumode_tc32_kernel<KC, true>, tc32::SMEM_BYTES, tc32::THREADS, tiles,
+                        "mumode_tc32_kernel (halves)", ahi, alo, b, mo, F, m, K, nl, st, max_pairs);
+  }
+  static int max_pairs = 0;
   return launch_pairs(mumode_tc32_kernel<KC>, tc32::SMEM_BYTES, tc32::THREADS, tiles, "mumode_tc32_kernel", ahi,
                       alo, b, mo, F, m, K, nl, st, max_pairs);
 }
@@ -90,9 +97,10 @@ int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t 
   if ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(ws)) & 15) return -1;
   if (K % 4 != 0 || m % 2 != 0 || m > (1 << 20) || K > (1 << 20)) return -1;
   if (reinterpret_cast<uintptr_t>(out) & 15) return -1;
-  // K' <= 512: one accumulation chain per tile (kmb200_tc32.cuh); longer
+  // K' <= 512: one accumulation chain per tile (kmb200_tc32.cuh); K' <= 1024: two
+  // chains of <= 512 k' summed in fp32 (the same kernel, HALVES); longer
   // contractions use the chunked kernel, whose chains stay at 64 k' (kmb200_tc32k.cuh)
-  const bool chunked = (kc ? 2 * K : K) > 512;
+  const bool chunked = (kc ? 2 * K : K) > (g_tc_halves_disabled ? 512 : 1024);
   const int64_t tile_fibers = (chunked ? tc32k::BNR : tc32::BNR) / 2;
   if (!kc && nl % tile_fibers != 0) return -1;  // a pair tile's fibers lie inside one slab
   if (F >= (int64_t(1) << 31)) return -1;

@@ -18,9 +18,15 @@
 // Both are exactly 4 real multiply-adds per complex multiply-add (x3 for the
 // split).  Accuracy: the tensor core's fp32 accumulation loses ~7e-9 relative
 // per accumulated k (measured: 1.0e-6 / 1.9e-6 / 3.7e-6 rel. l2 at K' = 128 /
-// 256 / 512 against complex128), so the host uses this kernel only up to
-// K' = 512 and keeps longer contractions on the DMMA path (1e-5 bar).  E's hi/lo planes are prepared once per call (prep_planes_kernel);
-// the tensor tile is split in shared memory by four transform warps.
+// 256 / 512 against complex128), so one accumulation chain stops at K' = 512.
+// HALVES (512 < K' <= 1024, e.g. direction 1 of a 512^3 state): the k-blocks of a
+// tile go to two chains, the first half into TMEM columns [0, 256), the second
+// into [256, 512); the epilogue folds the first into the second with fp32
+// round-to-nearest adds (tcgen05.ld / tcgen05.st) and releases it at once, so
+// the next tile's first half runs under the output pass.  Longer contractions
+// use the chunked kernel (kmb200_tc32k.cuh).  E's hi/lo planes are prepared
+// once per call (prep_planes_kernel); the tensor tile is split in shared memory
+// by four transform warps.
 //
 // CTA pairs (cta_group::2, cluster of 2): a tile is 256 real E rows x 256
 // tensor columns; each CTA stages its own 128 E rows and HALF of the tensor
@@ -136,6 +142,18 @@ __device__ __forceinline__ void ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};\n" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+      "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+      "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
 __device__ __forceinline__ float4 lds_f4(unsigned a) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
@@ -203,7 +221,7 @@ __global__ void prep_planes_kernel(const float2* __restrict__ L, float* __restri
   }
 }
 
-template <bool KC>
+template <bool KC, bool HALVES = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc32::THREADS, 1)
     mumode_tc32_kernel(const __grid_constant__ CUtensorMap mapAhi, const __grid_constant__ CUtensorMap mapAlo,
                        const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapOut, int64_t F,
@@ -288,12 +306,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc32::THREADS, 1)
     if (rank == 0 && lane == 0) {
       constexpr uint32_t idesc = idesc_tf32(!KC);
       int64_t q = 0;
+      // HALVES: k-blocks [0, KH) accumulate into columns [0, 256), [KH, KT) into
+      // [256, 512); whole tiles alternate between the two 256-column buffers
+      const int KH = (KT + 1) / 2;
       for (int64_t it = 0; it < my_tiles; ++it) {
-        const int b = static_cast<int>(it & 1);
-        if (it >= 2) tma::mbar_wait(&tempty[b], static_cast<unsigned>(((it >> 1) - 1) & 1));
+       for (int h = 0; h < (HALVES ? 2 : 1); ++h) {
+        const int b = HALVES ? h : static_cast<int>(it & 1);
+        if (HALVES ? it >= 1 : it >= 2)
+          tma::mbar_wait(&tempty[b], static_cast<unsigned>((HALVES ? it - 1 : (it >> 1) - 1) & 1));
         fence_after();
         const uint32_t d = tmem + b * BNR;
-        for (int kt = 0; kt < KT; ++kt, ++q) {
+        const int kb0 = HALVES && h ? KH : 0, kb1 = HALVES && !h ? KH : KT;
+        for (int kt = kb0; kt < kb1; ++kt, ++q) {
           const int s = static_cast<int>(q % ST);
           tma::mbar_wait(&ready[s], static_cast<unsigned>((q / ST) & 1));
           fence_after();
@@ -311,7 +335,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc32::THREADS, 1)
               bhi = desc_sw(st + OFF_B + ks * 1024, 2048, 512, 1);
               blo = desc_sw(st + OFF_BLO + ks * 1024, 2048, 512, 1);
             }
-            const uint32_t acc = (kt | ks) ? 1u : 0u;
+            const uint32_t acc = (kt != kb0 || ks) ? 1u : 0u;
             mma_tf32(d, ahi, bhi, idesc, acc);
             mma_tf32(d, alo, bhi, idesc, 1u);
             mma_tf32(d, ahi, blo, idesc, 1u);
@@ -319,6 +343,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc32::THREADS, 1)
           commit_pair(&empty[s]);
         }
         commit_pair(&tfull[b]);
+       }
       }
     }
   } else if (warp < 6) {
@@ -364,9 +389,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc32::THREADS, 1)
       const int64_t tile = pair + it * pairs;
       const int e0 = static_cast<int>(tile % nE) * 2 * BMR + static_cast<int>(rank) * BMR;
       const int64_t c0 = (tile / nE) * BNR;
-      const int b = static_cast<int>(it & 1);
-      tma::mbar_wait(&tfull[b], static_cast<unsigned>((it >> 1) & 1));
-      fence_after();
+      int b = static_cast<int>(it & 1);
+      if constexpr (HALVES) {
+        // fold the first half's accumulator into the second's (fp32 round-to-
+        // nearest adds, tcgen05.st) and release it at once, so the next tile's
+        // first half overlaps the output pass below
+        b = 1;
+        const uint32_t lanes = static_cast<uint32_t>(quarter * 32) << 16;
+        tma::mbar_wait(&tfull[0], static_cast<unsigned>(it & 1));
+        tma::mbar_wait(&tfull[1], static_cast<unsigned>(it & 1));
+        fence_after();
+#pragma unroll 1
+        for (int ch = 0; ch < BNR / 32; ++ch) {
+          float v0[32], v1[32];
+          ld32(tmem + lanes + ch * 32, v0);
+          ld32(tmem + lanes + BNR + ch * 32, v1);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v1[j] += v0[j];
+          st32(tmem + lanes + BNR + ch * 32, v1);
+        }
+        st_wait();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_leader(&tempty[0]);
+        fence_after();
+      } else {
+        tma::mbar_wait(&tfull[b], static_cast<unsigned>((it >> 1) & 1));
+        fence_after();
+      }
       const int nbase = (e0 >> 1) + quarter * 16;  // first output row (complex) of this warp
 #pragma unroll 1
       for (int ch = 0; ch < BNR / 32; ++ch) {

@@ -54,18 +54,31 @@ def test_c64_step_256_vs_oracle_and_dmma():
     assert orc.rel_l2(got, dmma) <= 1e-5
 
 
-@pytest.mark.parametrize("shape,mu", [((384, 64, 8), 1), ((512, 128, 8), 1), ((1024, 64, 4), 1),
-                                      ((128, 1024, 8), 2), ((128, 8, 1024), 3), ((256, 8, 640), 3)])
-def test_long_contractions_chunked_accumulation(shape, mu):
-    """K' > 512: the chunked tcgen05 kernel (fresh TMEM accumulator every 64 k', fp32 drain) keeps
-    the error at the short-contraction level instead of growing with K."""
+LONG = [((384, 64, 8), 1), ((512, 128, 8), 1), ((1024, 64, 4), 1), ((128, 1024, 8), 2), ((128, 8, 1024), 3),
+        ((256, 8, 640), 3), ((128, 8, 520), 3)]
+
+
+@pytest.mark.parametrize("shape,mu", LONG)
+@pytest.mark.parametrize("halves", [True, False])
+def test_long_contractions(shape, mu, halves):
+    """K' > 512.  Up to K' = 1024 the default is two accumulation chains of <= 512 k' per tile
+    summed in fp32 (HALVES): the error stays at the K' = 512 level of the production kernel
+    (measured 3.7e-6).  Beyond that, and for K' <= 1024 under KM_POLICY_NO_TC_HALVES, the
+    chunked kernel (fresh TMEM accumulator every 64 k', fp32 drain) keeps it lower."""
     rng = np.random.default_rng(sum(shape) + mu)
     u = crand(rng, shape)
     n = shape[mu - 1]
+    kp = 2 * n if mu == 1 else n
     mat = ((rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(n)).astype(np.complex64)
-    got = km.mu_mode_product(u, mat, mu)
+    lib = _native.lib()
+    try:
+        if not halves:
+            _native.check(lib.km_set_kernel_policy(_native.POLICY_NO_TC_HALVES))
+        got = km.mu_mode_product(u, mat, mu)
+    finally:
+        _native.check(lib.km_set_kernel_policy(_native.POLICY_AUTO))
     want128 = orc.mu_mode_product(u.astype(np.complex128), mat.astype(np.complex128), mu)
     want64 = orc.mu_mode_product(u, mat, mu)
     e128, e64 = orc.rel_l2(got, want128), orc.rel_l2(got, want64)
-    assert e128 <= 2e-6, e128
+    assert e128 <= (5e-6 if halves and kp <= 1024 else 2e-6), e128
     assert e64 <= 1e-5, e64

@@ -20,7 +20,10 @@ g = torch.Generator(device=dev).manual_seed(0)
 u = torch.randn((n, n, n), dtype=torch.complex64, device=dev, generator=g).permute(2, 1, 0)  # column-major
 rng = np.random.default_rng(0)
 mat = ((rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(n)).astype(np.complex64)
-for mu in (1, 2, 3):
+from paper_2103_01691_b200 import _native  # noqa: E402
+
+for mu, pol in ((1, _native.POLICY_AUTO), (1, _native.POLICY_NO_TC_HALVES), (2, 0), (3, 0)):
+    _native.check(_native.lib().km_set_kernel_policy(pol))
     km.mu_mode_product(u, mat, mu)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -30,4 +33,6 @@ for mu in (1, 2, 3):
     e1.record()
     e1.synchronize()
     ms = e0.elapsed_time(e1) / 5
-    print(f"n={n} mu={mu}: {ms:.3f} ms, {8 * n**4 / ms / 1e9:.1f} TFLOP/s complex")
+    tag = " (no halves: chunked)" if pol else ""
+    print(f"n={n} mu={mu}{tag}: {ms:.3f} ms, {8 * n**4 / ms / 1e9:.1f} TFLOP/s complex")
+_native.check(_native.lib().km_set_kernel_policy(_native.POLICY_AUTO))
