@@ -165,7 +165,7 @@ int pointwise_t(const void* in, void* out, int64_t n, const OpDev& op, cudaStrea
   if (split && op.inner > 0 && n % op.inner == 0) {
     // 2-D grid: x over directions 1..d-1, y over the last direction
     const int64_t nlast = n / op.inner;
-    int64_t bx = (op.inner + 4 * threads - 1) / (4 * threads);  // 4 elements per thread (pointwise_kernel)
+    int64_t bx = (op.inner + KMB_PW * threads - 1) / (KMB_PW * threads);  // KMB_PW elements per thread (pointwise_kernel)
     int64_t by = nlast;
     if (by > 65535) by = 65535;
     while (bx * by > cap && bx > 1) bx = (bx + 1) / 2;
