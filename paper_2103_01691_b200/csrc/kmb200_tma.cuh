@@ -166,21 +166,33 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
   auto sk_cta_of = [&](int64_t x) { return ((x + 1) * S + sk.iters - 1) / sk.iters - 1; };
 
   // one lane issues the loads of this CTA's k-block q
+  // producer cursor (leader lane only): issue() runs for q = 0, 1, 2, ... in
+  // order, so the k-block's tile and its TMA coordinates advance incrementally,
+  // with the 64-bit divisions done once per tile instead of once per k-block
+  int64_t pc_tile = cta, m0 = 0;
+  int kt = -1, n0 = 0, a_grp = 0, a_slab = 0;
+  auto set_tile = [&](int64_t tile) {
+    pc_tile = tile;
+    n0 = static_cast<int>(tile % nN) * BN;
+    m0 = (tile / nN) * BM;
+    if constexpr (!KC) {
+      a_grp = static_cast<int>((m0 % nl) / (CU ? 8 : 16));
+      a_slab = static_cast<int>(m0 / nl);
+    }
+  };
   auto issue = [&](int64_t q) {
     const int s = static_cast<int>(q % TSTAGES);
     if (q >= TSTAGES) tma::mbar_wait(&empty[s], static_cast<unsigned>((q / TSTAGES - 1) & 1));
-    int64_t tile;
-    int kt;
-    if (!SKT || q < n_dp * KT) {
-      tile = cta + (q / KT) * S;
-      kt = static_cast<int>(q % KT);
-    } else {
-      const int64_t gi = sk_b + (q - n_dp * KT);
-      tile = sk.sk_base + gi / KT;
-      kt = static_cast<int>(gi % KT);
+    if (SKT && q == n_dp * KT) {  // first k-block of the stream-K range
+      set_tile(sk.sk_base + sk_b / KT);
+      kt = static_cast<int>(sk_b % KT);
+    } else if (kt < 0) {
+      set_tile(cta);
+      kt = 0;
+    } else if (++kt == KT) {
+      kt = 0;
+      set_tile(SKT && q > n_dp * KT ? pc_tile + 1 : pc_tile + S);
     }
-    const int n0 = static_cast<int>(tile % nN) * BN;
-    const int64_t m0 = (tile / nN) * BM;
     unsigned char* st = smem + s * STAGE_BYTES;
     tma::mbar_expect_tx(&full[s], (CU ? A_BYTES : A_BYTES / 2) + (CL ? B_BYTES : B_BYTES / 2));
     const int k0 = kt * BKS;
@@ -188,14 +200,12 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
       tma::load3(st, &mapA, &full[s], k0, static_cast<int>(m0), 0);
     } else if constexpr (!CU) {
       const int kb = k0 / sp.kcb;
-      tma::load5(st, &mapA, &full[s], 0, k0 - kb * sp.kcb, static_cast<int>((m0 % nl) / 16), static_cast<int>(m0 / nl),
-                 kb);
+      tma::load5(st, &mapA, &full[s], 0, k0 - kb * sp.kcb, a_grp, a_slab, kb);
     } else if constexpr (KC) {
       tma::load3(st, &mapA, &full[s], 0, static_cast<int>(m0), k0 / 8);
     } else {
       const int kb = k0 / sp.kcb;
-      tma::load5(st, &mapA, &full[s], 0, k0 - kb * sp.kcb, static_cast<int>((m0 % nl) / 8), static_cast<int>(m0 / nl),
-                 kb);
+      tma::load5(st, &mapA, &full[s], 0, k0 - kb * sp.kcb, a_grp, a_slab, kb);
     }
     if constexpr (CL)
       tma::load3(st + A_BYTES, &mapB, &full[s], 0, n0, k0 / 8);
@@ -371,6 +381,10 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
     // epilogue (overlaps the producer's loads for the next tile)
     // fused ops run only where the host checked op_split_ok (inst_tma_c128.cu)
     const SplitOpCtx octx = split_ctx<OPK>(op);
+    // fiber-contiguous tiles lie inside one n_left slab (nl % BM == 0, host-checked):
+    // one 64-bit division per tile instead of one per output row
+    const int64_t f_q = KC ? 0 : m0 / nl;
+    const int64_t f_rem = KC ? 0 : m0 - f_q * nl, f_slab = KC ? 0 : f_q * nl * sp.ncb;
     // one 8-row block of the warp tile: row i (runtime) with accumulators crow/cirow
     // (with_op false: the values were already transformed, gpe_rows below)
     auto emit_row = [&](const int i, const double (&crow)[4][2], const double (&cirow)[4][2], const bool with_op) {
@@ -390,7 +404,7 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
           ob = f * N;
         }
       } else {
-        ob = (f % nl) + (f / nl) * nl * sp.ncb;
+        ob = f_rem + (f - m0) + f_slab;  // (f % nl) + (f / nl) * nl * ncb, f in this tile's slab
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
