@@ -109,6 +109,23 @@ int km_mumode(const void* u, int u_dtype, const void* L, int L_dtype, void* out,
               const km_pointop* post, void* stream);
 
 /*
+ * The trailing-direction product (n_right == 1) restricted to the output
+ * fibers [fiber0, fiber0 + fibers): out[f + i*n_left] for those f only, with u
+ * and out the full (n_left, n_mu) and (n_left, m) arrays.  Same arithmetic as
+ * km_mumode for those elements.  The host pipeline (_pipeline.py) uses it to
+ * finish the first output rows in fiber pieces, so their device-to-host copy
+ * starts before the whole row block is done (no reference counterpart: the
+ * reference's product is one np.matmul, tensor.py:136-139).
+ */
+int km_mumode_fibers(const void* u, int u_dtype, const void* L, int L_dtype, void* out, int64_t m,
+                     int64_t n_left, int64_t n_mu, int64_t fiber0, int64_t fibers, void* stream);
+
+/* cudaMemcpy2DAsync(cudaMemcpyDefault) on `stream`: `height` rows of `width`
+ * bytes; the host pipeline's strided device-to-host copies. */
+int km_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+               void* stream);
+
+/*
  * μ-mode product on blocked ("split") layouts — the fused pack/unpack of the
  * slab decomposition's all-to-all.  Same as km_mumode (n_left
  * must be > 1), except that

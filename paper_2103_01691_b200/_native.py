@@ -31,6 +31,8 @@ EXPORTS = (
     "km_last_error",
     "km_mumode",
     "km_mumode_split",
+    "km_mumode_fibers",
+    "km_copy_2d",
     "km_mumode_peer",
     "km_tucker",
     "km_tucker_workspace",
@@ -77,6 +79,10 @@ def _declare(lib):
     lib.km_mumode_split.restype = c_int
     lib.km_mumode_split.argtypes = [c_vp, c_int, c_vp, c_int, c_vp, c_i64, c_i64, c_i64, c_i64,
                                     ctypes.c_int32, c_i64, ctypes.c_int32, c_i64, c_vp]
+    lib.km_mumode_fibers.restype = c_int
+    lib.km_mumode_fibers.argtypes = [c_vp, c_int, c_vp, c_int, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp]
+    lib.km_copy_2d.restype = c_int
+    lib.km_copy_2d.argtypes = [c_vp, c_sz, c_vp, c_sz, c_sz, c_sz, c_vp]
     lib.km_mumode_peer.restype = c_int
     lib.km_mumode_peer.argtypes = [c_vp, c_int, c_vp, c_int, c_i64, c_i64, c_i64, c_i64, ctypes.c_int32, c_i64,
                                    ctypes.c_int32, c_i64, ctypes.POINTER(c_vp), ctypes.c_int32, c_i64, c_vp]

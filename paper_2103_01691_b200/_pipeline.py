@@ -30,6 +30,7 @@ from . import _device as dv
 from . import _native
 
 MIN_BYTES = 16 << 20
+FIB_PIECES = 4
 _streams = {}
 TRACE = []  # (label, event) of the last call when tracing is on (tools/e2e_timeline.py)
 _trace_on = False
@@ -225,7 +226,34 @@ def tucker_host_pipelined(host, u_dt, mats_dev, codes, rows, pre, post, out_shap
         row_bytes = dims[last] * _code_dtype(codes[last]).itemsize
         # row blocks of whole 64-row output tiles, so no launch pays for a padded tile
         parts2 = max(1, min(parts, rows[last] // 64)) if rows[last] >= 64 else 1
-        for (start, size) in _chunks(rows[last], parts2):
+        blocks = _chunks(rows[last], parts2)
+        # the first row block in FIB_PIECES fiber pieces (km_mumode_fibers), each shipped
+        # as a strided 2-D copy: the device-to-host copies start after ~1/FIB_PIECES of
+        # the block instead of all of it (256^3: 0.26 -> ~0.08 ms between the last H2D
+        # copy and the first D2H copy); double precision, no fused op
+        es_out = np.dtype(cdt).itemsize
+        piece = inner_mid // FIB_PIECES
+        double = (np.dtype(mid_dt) in (np.dtype(np.float64), np.dtype(np.complex128))
+                  and codes[last] in (_native.KM_F64, _native.KM_C128))
+        if (post is None and double and len(blocks) > 1 and inner_mid == inner_out
+                and inner_mid % FIB_PIECES == 0 and piece % 128 == 0):
+            start, size = blocks.pop(0)
+            lp = mats_dev[last].data_ptr() + start * row_bytes
+            for c in range(FIB_PIECES):
+                f0 = c * piece
+                _native.check(lib.km_mumode_fibers(mid_all.data_ptr(), dv.code(mid_dt), lp, codes[last],
+                                                   out_dev[inner_out * start:].data_ptr(), size, inner_mid,
+                                                   dims[last], f0, piece, stream_c))
+                _mark(f"dir {last + 1} rows {start}+{size} fibers {f0}+{piece}", compute)
+                ev = torch.cuda.Event()
+                ev.record(compute)
+                s_out.wait_event(ev)
+                off = (inner_out * start + f0) * es_out
+                _native.check(lib.km_copy_2d(host_out_flat.data_ptr() + off, inner_out * es_out,
+                                             out_dev.data_ptr() + off, inner_out * es_out, piece * es_out, size,
+                                             ctypes.c_void_p(s_out.cuda_stream)))
+                _mark(f"d2h rows {start} fibers {f0}", s_out)
+        for (start, size) in blocks:
             olo = inner_out * start
             dst = out_dev[olo: olo + inner_out * size]
             op = _op_for_slab(post, list(out_shape[:last]) + [size], last, start, size)

@@ -96,7 +96,8 @@ int num_sms() {
 int pointwise_impl(const void* in, void* out, int dt, int64_t n, const km_pointop* op, cudaStream_t st);
 
 int mumode_impl(const void* u, int udt, const void* L, int ldt, void* out, int64_t m, int64_t nl, int64_t nmu,
-                int64_t nr, const km_pointop* post, cudaStream_t st, const Split* split = nullptr) {
+                int64_t nr, const km_pointop* post, cudaStream_t st, const Split* split = nullptr,
+                int64_t fibers = -1) {
   if (udt < KM_F32 || udt > KM_C128 || ldt < KM_F32 || ldt > KM_C128)
     return fail(KM_EINVAL, "km_mumode: unknown dtype (u=%d, L=%d)", udt, ldt);
   if (is_double(udt) != is_double(ldt))
@@ -111,7 +112,9 @@ int mumode_impl(const void* u, int udt, const void* L, int ldt, void* out, int64
   if (post && post->kind != KM_OP_NONE && !(is_complex(udt) || is_complex(ldt)))
     return fail(KM_EINVAL, "km_mumode: pointwise op needs a complex result");
   const OpDev op = to_dev(post);
-  const int64_t M = nl * nr;
+  // fibers >= 0: only the first `fibers` fibers of an n_right == 1 product
+  // (km_mumode_fibers passes u and out already offset to its first fiber)
+  const int64_t M = fibers >= 0 ? fibers : nl * nr;
   const int N = static_cast<int>(m), K = static_cast<int>(nmu);
   Split sp{K, 0, N, 0};
   if (split) {
@@ -257,6 +260,27 @@ int km_mumode(const void* u, int u_dtype, const void* L, int L_dtype, void* out,
               int64_t n_mu, int64_t n_right, const km_pointop* post, void* stream) {
   return mumode_impl(u, u_dtype, L, L_dtype, out, m, n_left, n_mu, n_right, post,
                      static_cast<cudaStream_t>(stream));
+}
+
+int km_mumode_fibers(const void* u, int u_dtype, const void* L, int L_dtype, void* out, int64_t m, int64_t n_left,
+                     int64_t n_mu, int64_t fiber0, int64_t fibers, void* stream) {
+  if (u_dtype < KM_F32 || u_dtype > KM_C128 || L_dtype < KM_F32 || L_dtype > KM_C128)
+    return fail(KM_EINVAL, "km_mumode_fibers: unknown dtype (u=%d, L=%d)", u_dtype, L_dtype);
+  if (fiber0 < 0 || fibers < 1 || fiber0 + fibers > n_left)
+    return fail(KM_EINVAL, "km_mumode_fibers: fibers [%lld, %lld) outside [0, %lld)", (long long)fiber0,
+                (long long)(fiber0 + fibers), (long long)n_left);
+  if (!u || !out) return fail(KM_EINVAL, "km_mumode_fibers: NULL pointer");
+  const int64_t ue = elem_bytes(u_dtype), oe = elem_bytes(promote(u_dtype, L_dtype));
+  return mumode_impl(static_cast<const char*>(u) + fiber0 * ue, u_dtype, L, L_dtype,
+                     static_cast<char*>(out) + fiber0 * oe, m, n_left, n_mu, 1, nullptr,
+                     static_cast<cudaStream_t>(stream), nullptr, fibers);
+}
+
+int km_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height, void* stream) {
+  if (!dst || !src) return fail(KM_EINVAL, "km_copy_2d: NULL pointer");
+  const cudaError_t e =
+      cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDefault, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? KM_OK : fail(KM_ECUDA, "km_copy_2d: %s", cudaGetErrorString(e));
 }
 
 int km_mumode_split(const void* u, int u_dtype, const void* L, int L_dtype, void* out, int64_t m, int64_t n_left,

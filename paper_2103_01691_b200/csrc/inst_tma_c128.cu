@@ -184,7 +184,7 @@ int launch_tma_f64(const void* u, const void* L, void* out, int64_t M, int N, in
     cuuint32_t box[3] = {16, tma::BM, 2};
     if (!make_map(&ma, u, 3, dims, strides, box)) return -1;
   } else {
-    const int64_t nr = M / nl;
+    const int64_t nr = (M + nl - 1) / nl;  // M < nl: a fiber range of one slab (km_mumode_fibers)
     const int64_t nblk = (K + sp.kcb - 1) / sp.kcb;
     const int64_t es = complex_tensor ? 16 : 8;  // element bytes
     const int64_t kbs = nblk > 1 ? sp.kbs : static_cast<int64_t>(nl) * sp.kcb * nr;

@@ -104,3 +104,44 @@ def test_hermite_transforms_pipelined():
     assert orc.rel_l2(fwd, want) <= 1e-12
     back = km.inverse_transform((b,) * 3, fwd)
     assert orc.rel_l2(back, vals) <= 1e-11
+
+
+@pytest.mark.parametrize("cplx", [True, False])
+def test_mumode_fibers_matches_the_full_product(cplx):
+    """km_mumode_fibers (the first output row block in fiber pieces) writes exactly the
+    requested fibers of the trailing-direction product, bit for bit, and nothing else."""
+    import ctypes
+
+    import torch
+
+    from paper_2103_01691_b200 import _device as dv, _native
+
+    rng = np.random.default_rng(5)
+    shape, m = (64, 48, 40), 24
+    u = crand(rng, shape) if cplx else np.asfortranarray(rng.standard_normal(shape))
+    mat = rng.standard_normal((m, shape[2])) + (1j * rng.standard_normal((m, shape[2])) if cplx else 0)
+    dev = torch.device("cuda", 0)
+    code = _native.KM_C128 if cplx else _native.KM_F64
+    t = dv.to_device(u, u.dtype, dev)
+    L = torch.from_numpy(np.ascontiguousarray(mat)).to(dev)  # row-major, as the ABI takes factors
+    full = dv.to_host(km.mu_mode_product(t, L, 3)).reshape(-1, m, order="F")
+    nl = shape[0] * shape[1]
+    lib = _native.lib()
+    for f0, nf in [(0, nl), (128, 1000), (nl - 1, 1), (512, 1024)]:
+        out = torch.zeros(nl * m, dtype=t.dtype, device=dev)
+        _native.check(lib.km_mumode_fibers(t.data_ptr(), code, L.data_ptr(), code, out.data_ptr(), m, nl,
+                                           shape[2], f0, nf, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        got = out.cpu().numpy().reshape(nl, m, order="F")
+        assert np.array_equal(got[f0:f0 + nf], full[f0:f0 + nf])
+        assert not got[:f0].any() and not got[f0 + nf:].any()
+    with pytest.raises(Exception):
+        _native.check(lib.km_mumode_fibers(t.data_ptr(), code, L.data_ptr(), code, out.data_ptr(), m, nl,
+                                           shape[2], nl - 4, 8, None))
+
+
+def test_real_step_pipelined_vs_oracle():
+    rng = np.random.default_rng(6)
+    u = np.asfortranarray(rng.standard_normal((N, N, N)))
+    d2 = km.heat_factors(N, 2).factors[0]
+    cache = km.prepare(km.KroneckerOp((d2,) * 3), 1e-4)
+    assert orc.rel_l2(km.step(cache, u), orc.step(cache.exps, u)) <= 1e-12
