@@ -59,7 +59,9 @@ int launch_pairs(Kern kern, int smem, int threads, int64_t tiles, const char* wh
     max_pairs = n;
   }
   const int64_t pairs = tiles < max_pairs ? tiles : max_pairs;
-  kern<<<static_cast<unsigned>(2 * pairs), threads, smem, st>>>(ahi, alo, b, mo, F, m, K, nl);
+  const cudaError_t e = launch_pdl(kern, dim3(static_cast<unsigned>(2 * pairs)), dim3(threads), smem, st, ahi, alo,
+                                   b, mo, F, m, K, nl);
+  if (e != cudaSuccess) return fail(KM_ECUDA, "%s: %s", what, cudaGetErrorString(e));
   return check_launch(what);
 }
 
@@ -109,8 +111,9 @@ int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t 
     const int threads = 256;
     int64_t blocks = (m * K + threads - 1) / threads;
     if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
-    prep_planes_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(static_cast<const float2*>(L), planes,
-                                                                         static_cast<int>(m), static_cast<int>(K));
+    const cudaError_t e = launch_pdl(prep_planes_kernel, dim3(static_cast<unsigned>(blocks)), dim3(threads), 0, st,
+                                     static_cast<const float2*>(L), planes, static_cast<int>(m), static_cast<int>(K));
+    if (e != cudaSuccess) return fail(KM_ECUDA, "prep_planes_kernel: %s", cudaGetErrorString(e));
     int rc = check_launch("prep_planes_kernel");
     if (rc) return rc;
   }

@@ -193,6 +193,7 @@ __device__ __forceinline__ float tf32_hi(float x) {
 __global__ void prep_planes_kernel(const float2* __restrict__ L, float* __restrict__ planes, int m, int K) {
   const int64_t kc = static_cast<int64_t>(2 * m) * (2 * K);
   const int64_t mc = static_cast<int64_t>(2 * m) * K;
+  pdl_wait();  // the planes buffer may still be read by the previous product
   float* kc_hi = planes;
   float* kc_lo = planes + kc;
   float* mc_hi = planes + 2 * kc;
@@ -260,6 +261,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc32::THREADS, 1)
   fence_before();
   cluster_sync();  // barriers initialised and TMEM allocated in both CTAs before any remote arrive
   fence_after();
+  pdl_wait();  // the previous kernel (prep_planes_kernel, the previous product) is done
   const uint32_t tmem = *tmem_slot;
 
   const int64_t fib_r = KC ? F : 2 * F;                // real columns of B

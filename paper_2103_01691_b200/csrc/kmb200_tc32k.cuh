@@ -91,6 +91,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc32k::THREADS, 1)
   fence_before();
   tc32::cluster_sync();
   fence_after();
+  pdl_wait();  // the previous kernel (prep_planes_kernel, the previous product) is done
   const uint32_t tmem = *tmem_slot;
 
   const int64_t fib_r = KC ? F : 2 * F;
