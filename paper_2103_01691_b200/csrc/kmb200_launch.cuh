@@ -31,7 +31,7 @@ int launch_cfg(const void* u, const void* L, void* out, int64_t M, int N, int K,
 }
 
 // 128x64 tiles (8 warps) when they fill the machine at least twice over, else
-// 64x32 tiles (2 warps) so that small tensors still spread over all SMs.
+// smaller tiles so that small tensors still spread over all SMs.
 template <typename S, bool CU, bool CL, bool KC, int OPK>
 int launch_sized(const void* u, const void* L, void* out, int64_t M, int N, int K, int64_t nl, const OpDev& op,
                  const Split& sp, cudaStream_t st) {
@@ -39,6 +39,10 @@ int launch_sized(const void* u, const void* L, void* out, int64_t M, int N, int 
   if (big >= 2 * num_sms()) return launch_cfg<S, CU, CL, KC, OPK, 4, 2>(u, L, out, M, N, K, nl, op, sp, st);
   // small tensors: 32x32 tiles of four 16x16 warp tiles, ~4x the warps of the 64x32 variant
   const int64_t small = ((M + 31) / 32) * ((N + 31) / 32);
+  // fewer 32x32 tiles than SMs: 16x16 tiles of four 8x8 warp tiles (4x the warps again;
+  // tools/small_probe.py, 10 steps in a graph: 32^3 96 -> 64 us, 48^3 127 -> 111 us, while
+  // 64^3 is faster with the 32x32 tiles, 219 against 234 us)
+  if (small <= num_sms()) return launch_cfg<S, CU, CL, KC, OPK, 2, 2, 8>(u, L, out, M, N, K, nl, op, sp, st);
   if (small <= 16 * num_sms()) return launch_cfg<S, CU, CL, KC, OPK, 2, 2, 16>(u, L, out, M, N, K, nl, op, sp, st);
   return launch_cfg<S, CU, CL, KC, OPK, 2, 1>(u, L, out, M, N, K, nl, op, sp, st);
 }
