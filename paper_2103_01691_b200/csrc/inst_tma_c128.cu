@@ -80,7 +80,9 @@ int set_smem(Kern k) {
 // from 0.80 / 0.78 to 0.88 / 0.83 of the DMMA peak.  Between S/2 and S tiles
 // all k-blocks are cut into S ranges (tools/pipe_probe.py: the 1024^2 f64
 // pipe-flow step 189 -> 176 us, its complex128 variant 296 -> 283 us).
-// Many-wave launches measured no gain (1.2 % tail at 256^3).
+// Beyond 4 waves it is used only when the partial last wave wastes > 5 % of the
+// slots (160^3: 4.05 waves); the 256^3 headline (13.8 waves, 1.2 % tail) keeps
+// whole tiles.
 template <bool KC, int OPK, bool CL, bool CU>
 int launch_streamk(const CUtensorMap& ma, const CUtensorMap& mb, void* out, int64_t M, int N, int K, int64_t nl,
                    const OpDev& op, const Split& sp, cudaStream_t st) {
@@ -90,7 +92,11 @@ int launch_streamk(const CUtensorMap& ma, const CUtensorMap& mb, void* out, int6
   const int64_t S = num_sms();
   // fewer tiles than SMs (down to S/2): every k-block goes to the stream-K
   // range, a tile spans at most 3 CTAs (slots <= 2)
-  if (g_streamk_disabled || 2 * tiles < S || tiles % S == 0 || tiles > 4 * S || KT < 2) return -1;
+  if (g_streamk_disabled || 2 * tiles < S || tiles % S == 0 || KT < 2) return -1;
+  // many waves: only when the partial last wave wastes more than 5 % of the slots
+  // (256^3, 13.8 waves: 1.2 %, whole tiles; 160^3, 4.05 waves: 19 %)
+  const int64_t waves = (tiles + S - 1) / S;
+  if (tiles > 4 * S && 20 * (waves * S - tiles) <= waves * S) return -1;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(st, &cap);
   if (cap != cudaStreamCaptureStatusNone) return -1;  // epochs would repeat on replay
@@ -155,7 +161,11 @@ int launch_tma_f64(const void* u, const void* L, void* out, int64_t M, int N, in
   const int64_t tiles = ((M + tma::BM - 1) / tma::BM) * ((N + tma::BN - 1) / tma::BN);
   // persistent: worth it once the tiles cover ~3/4 of the SMs (smaller problems use
   // the cp.async kernel's 4x finer tiles)
+  // below two waves of tiles the cp.async kernel's finer tiles win unless K is long
+  // (tools/mid_probe.py: 96^3 step 105 -> 80 us, 128^3 230 -> 217 us; the 1024^2
+  // pipe-flow step, K = 1024, stays on this kernel)
   if (K % 8 != 0 || 4 * tiles < 3 * num_sms()) return -1;
+  if (tiles < 2 * num_sms() && K < 512) return -1;
   if ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(L)) & 15) return -1;
   if (!kc && (nl % tma::BM != 0 || (sp.kcb != K && sp.kcb % tma::BKS != 0))) return -1;
   if (static_cast<int64_t>(K) * 16 >= (int64_t(1) << 40) || M >= (int64_t(1) << 32)) return -1;
