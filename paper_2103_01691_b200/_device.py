@@ -157,24 +157,42 @@ def upload(arr, dev):
     if not (arr.flags.c_contiguous or f_order):
         arr = np.ascontiguousarray(arr)
     shape = arr.shape if not f_order else tuple(reversed(arr.shape))
-    out = torch.empty(shape, dtype=torch_dtype(arr.dtype), device=dev)
-    if f_order:
-        out = out.permute(*reversed(range(arr.ndim)))
     if nbytes == 0:
-        return out
+        out = torch.empty(shape, dtype=torch_dtype(arr.dtype), device=dev)
+        return out.permute(*reversed(range(arr.ndim))) if f_order else out
     entry = _staging_block(nbytes)
     stage = entry[0][:nbytes]
     stage.numpy()[:] = arr.ravel(order="K").view(np.uint8)
-    flat = out.permute(*reversed(range(arr.ndim))) if f_order else out
-    flat.view(-1).view(torch.uint8).copy_(stage, non_blocking=True)
-    entry[1] = torch.cuda.Event()
-    entry[1].record(torch.cuda.current_stream(dev))
-    return out
+    # the copy runs on a side stream into memory allocated from that stream's pool,
+    # so it overlaps the products already queued; the caller's stream waits for it
+    # (event) and the tensor is marked as used there (record_stream)
+    cur = torch.cuda.current_stream(dev)
+    side = _upload_stream(dev)
+    with torch.cuda.stream(side):
+        out = torch.empty(shape, dtype=torch_dtype(arr.dtype), device=dev)
+        out.view(-1).view(torch.uint8).copy_(stage, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(side)
+    cur.wait_event(done)
+    out.record_stream(cur)
+    entry[1] = done
+    return out.permute(*reversed(range(arr.ndim))) if f_order else out
+
+
+_UPLOAD_STREAMS = {}
+
+
+def _upload_stream(dev):
+    key = str(dev)
+    if key not in _UPLOAD_STREAMS:
+        _UPLOAD_STREAMS[key] = torch.cuda.Stream(dev)
+    return _UPLOAD_STREAMS[key]
 
 
 _STAGING = []  # ring of [pinned uint8 tensor, event of the copy that last read it (or None)]
 _STAGING_SLOTS = 16
 _STAGING_MIN = 1 << 20
+_STAGING_AHEAD = 4  # uploads of one size in flight before the host waits
 
 
 def _staging_block(nbytes):
@@ -187,7 +205,9 @@ def _staging_block(nbytes):
     for e in fits:
         if e[1] is None or e[1].query():
             return touch(e)
-    if len(_STAGING) < _STAGING_SLOTS or not fits:
+    # all fitting blocks busy: allocate another only while few fit (pinning host memory
+    # is slow and can stall the host for longer than the device work it would overlap)
+    if len(fits) < _STAGING_AHEAD and (len(_STAGING) < _STAGING_SLOTS or not fits):
         if len(_STAGING) >= _STAGING_SLOTS:  # no slot is large enough: retire the oldest
             old = _STAGING.pop(0)
             if old[1] is not None:

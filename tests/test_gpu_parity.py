@@ -339,6 +339,32 @@ def test_tdpot_strang_vs_oracle():
     assert rel(got, want) <= 1e-12
 
 
+@pytest.mark.parametrize("n,direction", [(32, 3), (256, 3), (48, 2), (40, 1)])
+def test_direction_diagonal_phase_ops(n, direction):
+    """KM_OP_DIAG as the pre pass and as the fused epilogue of the last product (the C-ABI op
+    behind direction-diagonal phases): psi -> f_b[i_dir] * (E-step(f_a[i_dir] * psi))."""
+    from paper_2103_01691_b200 import _device as dv
+    from paper_2103_01691_b200.problems import _diag_op
+    from paper_2103_01691_b200.tensor import run_tucker
+
+    rng = np.random.default_rng(n + direction)
+    shape = (n,) * 3
+    u = np.asfortranarray(rng.standard_normal(shape) + 1j * rng.standard_normal(shape))
+    mats = [(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(n) for _ in range(3)]
+    f_a = np.exp(1j * rng.standard_normal(n))
+    f_b = np.exp(1j * rng.standard_normal(n))
+    import torch
+
+    dev = torch.device("cuda", 0)
+    fa_d, fb_d = (dv.cached_vector(f, np.complex128, dev) for f in (f_a, f_b))
+    got = run_tucker(u, mats, pre=_diag_op(shape, fa_d, direction - 1), post=_diag_op(shape, fb_d, direction - 1),
+                     keepalive=(fa_d, fb_d))
+    bshape = [1, 1, 1]
+    bshape[direction - 1] = n
+    want = orc.step(mats, u * f_a.reshape(bshape)) * f_b.reshape(bshape)
+    assert rel(got, want) <= 1e-12
+
+
 def test_physical_propagator_equals_transform_step_transform():
     from paper_2103_01691_b200.hermite import physical_propagator
 
