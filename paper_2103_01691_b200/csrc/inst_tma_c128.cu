@@ -161,11 +161,12 @@ int launch_tma_f64(const void* u, const void* L, void* out, int64_t M, int N, in
   const int64_t tiles = ((M + tma::BM - 1) / tma::BM) * ((N + tma::BN - 1) / tma::BN);
   // persistent: worth it once the tiles cover ~3/4 of the SMs (smaller problems use
   // the cp.async kernel's 4x finer tiles)
-  // below two waves of tiles the cp.async kernel's finer tiles win unless K is long
-  // (tools/mid_probe.py: 96^3 step 105 -> 80 us, 128^3 230 -> 217 us; the 1024^2
-  // pipe-flow step, K = 1024, stays on this kernel)
+  // below two waves of tiles the cp.async kernel's finer tiles win for short K or
+  // padded row tiles (tools/mid_probe.py: 96^3 step 105 -> 80 us, 128^3 230 -> 216
+  // us); the stream-K cut keeps this kernel ahead for full-width tiles with K >= 256
+  // (P = 8 slab products, the 1024^2 pipe-flow step)
   if (K % 8 != 0 || 4 * tiles < 3 * num_sms()) return -1;
-  if (tiles < 2 * num_sms() && K < 512) return -1;
+  if (tiles < 2 * num_sms() && (K <= 128 || N % tma::BN != 0)) return -1;
   if ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(L)) & 15) return -1;
   if (!kc && (nl % tma::BM != 0 || (sp.kcb != K && sp.kcb % tma::BKS != 0))) return -1;
   if (static_cast<int64_t>(K) * 16 >= (int64_t(1) << 40) || M >= (int64_t(1) << 32)) return -1;
