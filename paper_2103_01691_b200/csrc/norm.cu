@@ -28,35 +28,33 @@ __global__ void __launch_bounds__(NORM_THREADS) norm_partial_kernel(const T* __r
   const int64_t stride = static_cast<int64_t>(gridDim.x) * NORM_THREADS;
   int64_t i = blockIdx.x * static_cast<int64_t>(NORM_THREADS) + threadIdx.x;
   if constexpr (KIND == 2) {
-    // (l, i_last) = (i mod inner, i / inner) advanced incrementally: one
-    // division per thread instead of one per element
+    // 2-D walk (norm_grid2): x over l = the directions 1..d-1 (U coalesced
+    // columns per thread, their inner weights loaded once), y over i_last (its
+    // weight loaded once per row); the weight product is w_inner[l] * w_last
+    // as in the reference (problems.py:528-539).  Fixed order per thread.
+    constexpr int U = 4;
     const double* wl = w.w[w.d - 1];
-    const int64_t qs = stride / w.inner, rs = stride - qs * w.inner;
-    int64_t il = i / w.inner, l = i - il * w.inner;
-    auto advance = [&](int64_t& l_, int64_t& il_) {
-      l_ += rs;
-      il_ += qs;
-      if (l_ >= w.inner) {
-        l_ -= w.inner;
-        ++il_;
-      }
-    };
-    for (; i + 3 * stride < n; i += 4 * stride) {  // four elements in flight, fixed fold order
-      double2 x[4];
-      double wt[4];
+    const int64_t nlast = n / w.inner;
+    for (int64_t l0 = blockIdx.x * static_cast<int64_t>(NORM_THREADS * U) + threadIdx.x; l0 < w.inner;
+         l0 += static_cast<int64_t>(gridDim.x) * NORM_THREADS * U) {
+      double wf[U];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        x[j] = load_diff(a, b, i + j * stride);
-        wt[j] = __ldg(w.winner + l) * __ldg(wl + il);
-        advance(l, il);
+      for (int u = 0; u < U; ++u) {
+        const int64_t l = l0 + u * NORM_THREADS;
+        wf[u] = l < w.inner ? __ldg(w.winner + l) : 0.0;
       }
+      for (int64_t il = blockIdx.y; il < nlast; il += gridDim.y) {
+        const double wlast = __ldg(wl + il);
+        const int64_t base = il * w.inner;
+        double2 x[U];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc += (x[j].x * x[j].x + x[j].y * x[j].y) * wt[j];
-    }
-    for (; i < n; i += stride) {
-      const double2 x = load_diff(a, b, i);
-      acc += (x.x * x.x + x.y * x.y) * (__ldg(w.winner + l) * __ldg(wl + il));
-      advance(l, il);
+        for (int u = 0; u < U; ++u) {
+          const int64_t l = l0 + u * NORM_THREADS;
+          x[u] = l < w.inner ? load_diff(a, b, base + l) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc += (x[u].x * x[u].x + x[u].y * x[u].y) * (wf[u] * wlast);
+      }
     }
   } else {
     // four independent loads in flight per thread, folded in a fixed order
@@ -87,7 +85,7 @@ __global__ void __launch_bounds__(NORM_THREADS) norm_partial_kernel(const T* __r
   if (threadIdx.x == 0) {
     double r = red[0];
     for (int k = 1; k < NORM_THREADS / 32; ++k) r = KIND == 0 ? fmax(r, red[k]) : r + red[k];
-    partials[blockIdx.x] = r;
+    partials[blockIdx.y * gridDim.x + blockIdx.x] = r;
   }
 }
 
@@ -107,11 +105,25 @@ __global__ void norm_final_kernel(const double* __restrict__ partials, int np, d
 
 int norm_blocks() { return 4 * num_sms(); }
 
+// weighted_two grid: x blocks over the inner index (<= what 4 coalesced columns per
+// thread need), y blocks over the last direction, x * y <= norm_blocks() partials
+dim3 norm_grid2(const OpDev& w, int64_t n) {
+  const int nb = norm_blocks();
+  int64_t gx = (w.inner + NORM_THREADS * 4 - 1) / (NORM_THREADS * 4);
+  if (gx > nb) gx = nb;
+  int64_t gy = nb / gx;
+  const int64_t nlast = n / w.inner;
+  if (gy > nlast) gy = nlast;
+  if (gy > 65535) gy = 65535;
+  return dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
+}
+
 template <typename T, int KIND>
 int norm_t(const void* a, const void* b, int64_t n, const OpDev& w, double* out, double* ws, cudaStream_t st) {
-  const int nb = norm_blocks();
-  norm_partial_kernel<T, KIND><<<nb, NORM_THREADS, 0, st>>>(static_cast<const T*>(a), static_cast<const T*>(b), n, w,
-                                                             ws);
+  const dim3 grid = KIND == 2 ? norm_grid2(w, n) : dim3(norm_blocks());
+  const int nb = static_cast<int>(grid.x * grid.y);
+  norm_partial_kernel<T, KIND><<<grid, NORM_THREADS, 0, st>>>(static_cast<const T*>(a), static_cast<const T*>(b), n,
+                                                               w, ws);
   norm_final_kernel<KIND><<<1, 32, 0, st>>>(ws, nb, out);
   return check_launch("norm kernels");
 }
