@@ -120,6 +120,17 @@ int km_mumode(const void* u, int u_dtype, const void* L, int L_dtype, void* out,
 int km_mumode_fibers(const void* u, int u_dtype, const void* L, int L_dtype, void* out, int64_t m,
                      int64_t n_left, int64_t n_mu, int64_t fiber0, int64_t fibers, void* stream);
 
+/*
+ * Configuration 4's potential flows folded into a complex128 propagator:
+ * out[i][j] = exp(-i x_rows[i] c_b) * E[i][j] * exp(-i x_cols[j] c_a), E and
+ * out row-major m x k (not overlapping), x_* device node vectors, c_a / c_b
+ * the integrals of sin^2 over the two half steps.  The Strang step of
+ * problems.tdpot_strang_step is then a plain km_tucker launch (no reference
+ * counterpart: the reference has no configuration-4 driver).
+ */
+int km_diag_phase_fold(const void* E, void* out, int64_t m, int64_t k, const double* x_rows, const double* x_cols,
+                       double c_a, double c_b, void* stream);
+
 /* cudaMemcpy2DAsync(cudaMemcpyDefault) on `stream`: `height` rows of `width`
  * bytes; the host pipeline's strided device-to-host copies. */
 int km_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,

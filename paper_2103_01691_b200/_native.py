@@ -33,6 +33,7 @@ EXPORTS = (
     "km_mumode_split",
     "km_mumode_fibers",
     "km_copy_2d",
+    "km_diag_phase_fold",
     "km_mumode_peer",
     "km_tucker",
     "km_tucker_workspace",
@@ -81,6 +82,8 @@ def _declare(lib):
                                     ctypes.c_int32, c_i64, ctypes.c_int32, c_i64, c_vp]
     lib.km_mumode_fibers.restype = c_int
     lib.km_mumode_fibers.argtypes = [c_vp, c_int, c_vp, c_int, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp]
+    lib.km_diag_phase_fold.restype = c_int
+    lib.km_diag_phase_fold.argtypes = [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, ctypes.c_double, ctypes.c_double, c_vp]
     lib.km_copy_2d.restype = c_int
     lib.km_copy_2d.argtypes = [c_vp, c_sz, c_vp, c_sz, c_sz, c_sz, c_vp]
     lib.km_mumode_peer.restype = c_int

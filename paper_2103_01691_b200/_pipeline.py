@@ -31,6 +31,7 @@ from . import _native
 
 MIN_BYTES = 16 << 20
 FIB_PIECES = 4
+TAIL_SHIFTS = (3, 4, 5, 6)  # last input slabs: n/8, n/16, n/32, n/64
 _streams = {}
 TRACE = []  # (label, event) of the last call when tracing is on (tools/e2e_timeline.py)
 _trace_on = False
@@ -63,9 +64,9 @@ def _input_slabs(n, parts):
     finish while the next, half-size slab is still in flight, and only the
     smallest slab's products remain when the copies end.  The rest is uniform.
     """
-    if parts < 6 or n < 16 * parts:
+    if parts < len(TAIL_SHIFTS) + 2 or n < 16 * parts:
         return _chunks(n, parts)
-    tail = [max(1, n >> s) for s in (3, 4, 5, 6)]
+    tail = [max(1, n >> s) for s in TAIL_SHIFTS]
     head = _chunks(n - sum(tail), parts - len(tail))
     out, start = list(head), n - sum(tail)
     for size in tail:

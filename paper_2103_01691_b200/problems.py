@@ -207,10 +207,10 @@ def tdpot_strang_step(linear_cache, x_nodes, psi, t, tau, direction=3):
     flow ``exp(-i x ∫ sin^2)`` over [t, t+tau/2] is applied before and over
     [t+tau/2, t+tau] after it.  Both flows are diagonal along ``direction``
     and the products along the other directions commute with them, so they
-    are folded into that direction's propagator on the host,
-    ``diag(f_b) E diag(f_a)`` (an n x n scaling, uploaded asynchronously),
-    and the step is a plain d-product Tucker launch: no pointwise pass at
-    all.  Against applying the two phases separately the results differ
+    are folded into that direction's propagator on the device,
+    ``diag(f_b) E diag(f_a)`` (``km_diag_phase_fold``: the phases are formed
+    from the node vector and two scalars, nothing is uploaded per step), and
+    the step is a plain d-product Tucker launch: no pointwise pass at all.  Against applying the two phases separately the results differ
     only in rounding (tests/test_gpu_parity.py).
     """
     po = _Operand(psi)
@@ -224,8 +224,7 @@ def tdpot_strang_step(linear_cache, x_nodes, psi, t, tau, direction=3):
                          f"{po.shape[direction - 1]}")
     out_dtype = _strang_dtype(po.dtype, linear_cache)
     dev = po.obj.device if po.is_tensor and po.obj.is_cuda else dv.device()
-    f_a = tdpot_phase_factor(x, t, t + 0.5 * tau)
-    f_b = tdpot_phase_factor(x, t + 0.5 * tau, t + tau)
+    c_a, c_b = sin2_integral(t, t + 0.5 * tau), sin2_integral(t + 0.5 * tau, t + tau)
     state = po.obj
     if po.dtype != out_dtype and not po.is_tensor:
         state = np.asarray(state).astype(out_dtype, order="F")
@@ -233,9 +232,14 @@ def tdpot_strang_step(linear_cache, x_nodes, psi, t, tau, direction=3):
         state = dv.tensor_as(state, out_dtype)
     mats = _cache_mats(linear_cache, _Operand(state))
     k = direction - 1
-    folded = (f_b[:, None] * np.asarray(linear_cache.exps[k])) * f_a[None, :]
-    mats[k] = dv.upload(np.ascontiguousarray(folded, dtype=dv.np_dtype(mats[k].dtype)), dev)
-    return run_tucker(state, mats, out_dtype=out_dtype)
+    e = mats[k] if mats[k].dtype == dv.torch.complex128 else mats[k].to(dv.torch.complex128)
+    x_dev = dv.cached_vector(x, np.float64, dev)
+    folded = dv.torch.empty_like(e)
+    _native.check(_native.lib().km_diag_phase_fold(e.data_ptr(), folded.data_ptr(), e.shape[0], e.shape[1],
+                                                   x_dev.data_ptr(), x_dev.data_ptr(), c_a, c_b,
+                                                   dv.stream_ptr(dev)))
+    mats[k] = folded
+    return run_tucker(state, mats, out_dtype=out_dtype, keepalive=(x_dev, e))
 
 
 def magnus_midpoint_step(factors_of_t, u, t, tau, device_expm=False):
