@@ -29,17 +29,16 @@ _NP_TO_CODE = {
 SUPPORTED = tuple(_NP_TO_CODE)
 
 
-def torch_dtype(np_dtype):
-    return {
+_NP_TO_TORCH = {}
+_TORCH_TO_NP = {}
+if torch is not None:
+    _NP_TO_TORCH = {
         np.dtype(np.float32): torch.float32,
         np.dtype(np.float64): torch.float64,
         np.dtype(np.complex64): torch.complex64,
         np.dtype(np.complex128): torch.complex128,
-    }[np.dtype(np_dtype)]
-
-
-def np_dtype(t_dtype):
-    return {
+    }
+    _TORCH_TO_NP = {
         torch.float32: np.dtype(np.float32),
         torch.float64: np.dtype(np.float64),
         torch.complex64: np.dtype(np.complex64),
@@ -48,7 +47,15 @@ def np_dtype(t_dtype):
         torch.int64: np.dtype(np.int64),
         torch.int32: np.dtype(np.int32),
         torch.bool: np.dtype(np.bool_),
-    }[t_dtype]
+    }
+
+
+def torch_dtype(np_dtype):
+    return _NP_TO_TORCH[np.dtype(np_dtype)]
+
+
+def np_dtype(t_dtype):
+    return _TORCH_TO_NP[t_dtype]
 
 
 def code(np_dt):
@@ -66,7 +73,16 @@ def device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_raw_stream = getattr(getattr(torch, "_C", None), "_cuda_getCurrentRawStream", None) if torch is not None else None
+
+
 def stream_ptr(dev=None):
+    """The current CUDA stream of ``dev`` as a C pointer (the fast raw-stream query when
+    this torch build has it: a public ``current_stream`` lookup costs a few microseconds)."""
+    if _raw_stream is not None:
+        idx = torch.cuda.current_device() if dev is None else (dev.index if isinstance(dev, torch.device) else int(dev))
+        if idx is not None:
+            return ctypes.c_void_p(_raw_stream(idx))
     return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
 
 
@@ -301,6 +317,8 @@ def cached_vector(v, dtype, dev):
     complex64 factor, on the critical path of every mu_mode_product call).
     """
     if is_tensor(v):
+        if v.device == dev and v.dtype == torch_dtype(dtype) and v.is_contiguous():
+            return v
         return v.to(device=dev, dtype=torch_dtype(dtype)).contiguous()
     src = np.asarray(v)
     if not (src.flags.c_contiguous or src.flags.f_contiguous):
