@@ -383,6 +383,8 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
     const SplitOpCtx octx = split_ctx<OPK>(op);
     // fiber-contiguous tiles lie inside one n_left slab (nl % BM == 0, host-checked):
     // one 64-bit division per tile instead of one per output row
+    // output rows in one block (no slab split, no peers): no per-column block division
+    const bool plain_rows = sp.ncb >= N && !sp.peer[0];
     const int64_t f_q = KC ? 0 : m0 / nl;
     const int64_t f_rem = KC ? 0 : m0 - f_q * nl, f_slab = KC ? 0 : f_q * nl * sp.ncb;
     // one 8-row block of the warp tile: row i (runtime) with accumulators crow/cirow
@@ -409,7 +411,7 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int c8 = n0 + wn + j * 8;
-        const int nblk = KC ? 0 : c8 / sp.ncb;
+        const int nblk = (KC || plain_rows) ? 0 : c8 / sp.ncb;
         TO* dst = obase;
         int64_t obj = ob - static_cast<int64_t>(nblk) * sp.ncb * cs;
         if (!KC && sp.peer[0]) dst = static_cast<TO*>(sp.peer[nblk]) + sp.peer_off;
