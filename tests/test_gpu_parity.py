@@ -365,6 +365,35 @@ def test_direction_diagonal_phase_ops(n, direction):
     assert rel(got, want) <= 1e-12
 
 
+@pytest.mark.parametrize("m,k,same", [(24, 40, False), (64, 64, True)])
+def test_diag_phase_fold_matches_numpy(m, k, same):
+    """km_diag_phase_fold (config 4's flows folded into a factor) against the host formula
+    (f_b[i] * E[i, j]) * f_a[j] with f = exp(-1j * x * c)."""
+    import ctypes
+
+    import torch
+
+    from paper_2103_01691_b200 import _device as dv, _native
+
+    rng = np.random.default_rng(m + k)
+    E = rng.standard_normal((m, k)) + 1j * rng.standard_normal((m, k))
+    xr = rng.standard_normal(m) * 3
+    xc = xr if same else rng.standard_normal(k) * 3
+    c_a, c_b = 0.0123, 0.0456
+    dev_ = torch.device("cuda", 0)
+    e_d = torch.from_numpy(E).to(dev_)
+    out = torch.empty_like(e_d)
+    xr_d, xc_d = torch.from_numpy(xr).to(dev_), torch.from_numpy(xc).to(dev_)
+    _native.check(_native.lib().km_diag_phase_fold(e_d.data_ptr(), out.data_ptr(), m, k, xr_d.data_ptr(),
+                                                   xc_d.data_ptr(), c_a, c_b,
+                                                   ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    want = (np.exp(-1j * xr * c_b)[:, None] * E) * np.exp(-1j * xc * c_a)[None, :]
+    assert rel(out.cpu().numpy(), want) <= 1e-15
+    with pytest.raises(Exception):
+        _native.check(_native.lib().km_diag_phase_fold(e_d.data_ptr(), e_d.data_ptr(), m, k, xr_d.data_ptr(),
+                                                       xc_d.data_ptr(), c_a, c_b, None))
+
+
 def test_physical_propagator_equals_transform_step_transform():
     from paper_2103_01691_b200.hermite import physical_propagator
 

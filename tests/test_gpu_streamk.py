@@ -83,6 +83,23 @@ def test_streamk_mixed_dtypes(shape, mu, mix):
     assert orc.rel_l2(a, b) <= 1e-14
 
 
+# beyond 4 waves stream-K runs only when the last wave wastes > 5 % of the slots:
+# (160,160,160) has 200 x 3 = 600 tiles (4.05 waves, 19 % waste; K = 160) -> stream-K,
+# (192,192,192) has 288 x 3 = 864 (5.84 waves, 2.7 %) -> whole tiles
+@pytest.mark.parametrize("shape,mu", [((160, 160, 160), 1), ((160, 160, 160), 3), ((192, 192, 192), 3)])
+def test_streamk_many_waves(shape, mu):
+    rng = np.random.default_rng(sum(shape) + mu)
+    u = crand(rng, shape)
+    n = shape[mu - 1]
+    mat = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    t = dev(u)
+    a, b = policies(lambda: dv.to_host(km.mu_mode_product(t, mat, mu)))
+    want = orc.mu_mode_product(u, mat, mu)
+    assert orc.rel_l2(a, want) <= 1e-13
+    assert orc.rel_l2(b, want) <= 1e-13
+    assert orc.rel_l2(a, b) <= 1e-14
+
+
 def test_streamk_repeated_launches_are_deterministic():
     rng = np.random.default_rng(7)
     u = dev(crand(rng, (256, 256, 32)))
