@@ -37,6 +37,9 @@
 
 namespace kmb {
 
+#ifndef KMB_EPI_VEC
+#define KMB_EPI_VEC 8
+#endif
 #ifndef KMB_TMA_AHEAD
 #define KMB_TMA_AHEAD 2
 #endif
@@ -450,19 +453,25 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
       for (int i = 0; i < 4; ++i) {
         const int64_t f = m0 + wm + i * 8 + g;
         const double lf = f < M ? split_fiber_weight<OPK>(op, f) : 1.0;
-        double w[8], vr[8], vi[8];
+        constexpr int EV = KMB_EPI_VEC;  // elements per gpe_rotate_vec call
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          w[e] = __dmul_rn(lf, wl[e >> 1][e & 1]);
-          vr[e] = cr[0][e >> 1][e & 1];
-          vi[e] = ci[0][e >> 1][e & 1];
-        }
-        gpe_rotate_vec<8>(op.coef, w, vr, vi);
-        if (op.repeat > 1) gpe_rotate_vec<8>(op.coef, w, vr, vi);
+        for (int hv = 0; hv < 8 / EV; ++hv) {
+          double w[EV], vr[EV], vi[EV];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          cr[0][e >> 1][e & 1] = vr[e];
-          ci[0][e >> 1][e & 1] = vi[e];
+          for (int e = 0; e < EV; ++e) {
+            const int x = hv * EV + e;
+            w[e] = __dmul_rn(lf, wl[x >> 1][x & 1]);
+            vr[e] = cr[0][x >> 1][x & 1];
+            vi[e] = ci[0][x >> 1][x & 1];
+          }
+          gpe_rotate_vec<EV>(op.coef, w, vr, vi);
+          if (op.repeat > 1) gpe_rotate_vec<EV>(op.coef, w, vr, vi);
+#pragma unroll
+          for (int e = 0; e < EV; ++e) {
+            const int x = hv * EV + e;
+            cr[0][x >> 1][x & 1] = vr[e];
+            ci[0][x >> 1][x & 1] = vi[e];
+          }
         }
         emit_row(i, cr[0], ci[0], false);
 #pragma unroll
