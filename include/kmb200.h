@@ -177,10 +177,14 @@ int km_mumode_peer(const void* u, int u_dtype, const void* L, int L_dtype, int64
  * complex64 x complex64 μ-mode product on the 5th-generation tensor cores
  * (tcgen05.mma kind::tf32, TMEM accumulator, 3xTF32 split for fp32-level
  * accuracy).  Same arguments as km_mumode plus a device workspace of at least
- * km_tc_workspace_bytes(m, n_mu) bytes (the factor's split planes).  Shapes
- * the kernel does not take (n_left > 1 with n_left % 128 != 0, n_mu % 4 != 0,
- * a contraction K' = 2*n_mu (n_left == 1) or n_mu (n_left > 1) above 512,
- * a too-small workspace, KM_POLICY_NO_TMA) run the DMMA path instead.
+ * km_tc_workspace_bytes(m, n_mu) bytes (the factor's split planes).  The
+ * contraction K' = 2*n_mu (n_left == 1) or n_mu (n_left > 1) runs as one
+ * accumulation chain up to 512, as two folded chains up to 1024, and in
+ * 64-k' chunks beyond (the tensor core's fp32 accumulation truncates, so a
+ * chain's error grows with its length).  Shapes the kernels do not take
+ * (n_left > 1 with n_left % 128 != 0 (% 64 for the chunked kernel),
+ * n_mu % 4 != 0, odd m, a too-small workspace, KM_POLICY_NO_TMA) run the
+ * DMMA path instead.
  */
 int km_tc_workspace_bytes(int64_t m, int64_t n_mu, size_t* bytes);
 int km_mumode_c64_tc(const void* u, const void* L, void* out, int64_t m, int64_t n_left,
