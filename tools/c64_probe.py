@@ -1,4 +1,4 @@
-"""complex64 exact steps on tcgen05 at 256^3 and 512^3 (512: direction 1 runs the chunked kernel),
+"""complex64 exact steps on tcgen05 at 256^3 and 512^3 (512: direction 1, K' = 1024, runs two folded accumulation chains),
 device time per step and parity against the complex128 and complex64 oracle steps."""
 import os
 import sys

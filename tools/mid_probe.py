@@ -1,3 +1,8 @@
+"""Mid-size exact steps (96^3 .. 192^3, rectangular, 2048^2): device time per step (LocalStepper,
+CUDA events) and per-direction launch times, for the cp.async / TMA / stream-K kernel choice.
+
+    python tools/mid_probe.py
+"""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch

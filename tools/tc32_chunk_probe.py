@@ -1,4 +1,5 @@
-"""One long-contraction complex64 product (direction 1 of 512^3: K' = 1024, chunked tcgen05 kernel)."""
+"""One long-contraction complex64 product (direction 1 of n x n x 64, K' = 2n): the HALVES kernel up to
+K' = 1024, the chunked tcgen05 kernel beyond (or under KM_POLICY_NO_TC_HALVES)."""
 import os
 import sys
 
