@@ -312,40 +312,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc32::THREADS, 1)
       // [256, 512); whole tiles alternate between the two 256-column buffers
       const int KH = (KT + 1) / 2;
       for (int64_t it = 0; it < my_tiles; ++it) {
-       for (int h = 0; h < (HALVES ? 2 : 1); ++h) {
-        const int b = HALVES ? h : static_cast<int>(it & 1);
-        if (HALVES ? it >= 1 : it >= 2)
-          tma::mbar_wait(&tempty[b], static_cast<unsigned>((HALVES ? it - 1 : (it >> 1) - 1) & 1));
-        fence_after();
-        const uint32_t d = tmem + b * BNR;
-        const int kb0 = HALVES && h ? KH : 0, kb1 = HALVES && !h ? KH : KT;
-        for (int kt = kb0; kt < kb1; ++kt, ++q) {
-          const int s = static_cast<int>(q % ST);
-          tma::mbar_wait(&ready[s], static_cast<unsigned>((q / ST) & 1));
+        for (int h = 0; h < (HALVES ? 2 : 1); ++h) {
+          const int b = HALVES ? h : static_cast<int>(it & 1);
+          if (HALVES ? it >= 1 : it >= 2)
+            tma::mbar_wait(&tempty[b], static_cast<unsigned>((HALVES ? it - 1 : (it >> 1) - 1) & 1));
           fence_after();
-          const unsigned st = sbase + s * STAGE_BYTES;
+          const uint32_t d = tmem + b * BNR;
+          const int kb0 = HALVES && h ? KH : 0, kb1 = HALVES && !h ? KH : KT;
+          for (int kt = kb0; kt < kb1; ++kt, ++q) {
+            const int s = static_cast<int>(q % ST);
+            tma::mbar_wait(&ready[s], static_cast<unsigned>((q / ST) & 1));
+            fence_after();
+            const unsigned st = sbase + s * STAGE_BYTES;
 #pragma unroll
-          for (int ks = 0; ks < BKR / 8; ++ks) {
-            // A (E planes): K-major SW64 (8 rows x 64 B atoms, 512 B apart); 8 k = 32 B per step
-            const uint64_t ahi = desc_sw(st + ks * 32, 16, 512, 4);
-            const uint64_t alo = desc_sw(st + OFF_ALO + ks * 32, 16, 512, 4);
-            uint64_t bhi, blo;
-            if constexpr (KC) {  // K-major like A
-              bhi = desc_sw(st + OFF_B + ks * 32, 16, 512, 4);
-              blo = desc_sw(st + OFF_BLO + ks * 32, 16, 512, 4);
-            } else {  // MN-major: 32-float column chunks 2048 B apart (LBO), 4-k groups 512 B apart (SBO)
-              bhi = desc_sw(st + OFF_B + ks * 1024, 2048, 512, 1);
-              blo = desc_sw(st + OFF_BLO + ks * 1024, 2048, 512, 1);
+            for (int ks = 0; ks < BKR / 8; ++ks) {
+              // A (E planes): K-major SW64 (8 rows x 64 B atoms, 512 B apart); 8 k = 32 B per step
+              const uint64_t ahi = desc_sw(st + ks * 32, 16, 512, 4);
+              const uint64_t alo = desc_sw(st + OFF_ALO + ks * 32, 16, 512, 4);
+              uint64_t bhi, blo;
+              if constexpr (KC) {  // K-major like A
+                bhi = desc_sw(st + OFF_B + ks * 32, 16, 512, 4);
+                blo = desc_sw(st + OFF_BLO + ks * 32, 16, 512, 4);
+              } else {  // MN-major: 32-float column chunks 2048 B apart (LBO), 4-k groups 512 B apart (SBO)
+                bhi = desc_sw(st + OFF_B + ks * 1024, 2048, 512, 1);
+                blo = desc_sw(st + OFF_BLO + ks * 1024, 2048, 512, 1);
+              }
+              const uint32_t acc = (kt != kb0 || ks) ? 1u : 0u;
+              mma_tf32(d, ahi, bhi, idesc, acc);
+              mma_tf32(d, alo, bhi, idesc, 1u);
+              mma_tf32(d, ahi, blo, idesc, 1u);
             }
-            const uint32_t acc = (kt != kb0 || ks) ? 1u : 0u;
-            mma_tf32(d, ahi, bhi, idesc, acc);
-            mma_tf32(d, alo, bhi, idesc, 1u);
-            mma_tf32(d, ahi, blo, idesc, 1u);
+            commit_pair(&empty[s]);
           }
-          commit_pair(&empty[s]);
+          commit_pair(&tfull[b]);
         }
-        commit_pair(&tfull[b]);
-       }
       }
     }
   } else if (warp < 6) {
