@@ -22,6 +22,7 @@ offset to the slab's first index.  Results are identical to the unpipelined
 from __future__ import annotations
 
 import ctypes
+import time
 from math import prod
 
 import numpy as np
@@ -33,7 +34,7 @@ MIN_BYTES = 16 << 20
 FIB_PIECES = 4
 TAIL_SHIFTS = (3, 4, 5, 6)  # last input slabs: n/8, n/16, n/32, n/64
 _streams = {}
-TRACE = []  # (label, event) of the last call when tracing is on (tools/e2e_timeline.py)
+TRACE = []  # (label, event, host time) of the last call when tracing is on (tools/e2e_timeline.py)
 _trace_on = False
 
 
@@ -100,7 +101,7 @@ def _mark(label, stream):
     if _trace_on:
         ev = dv.torch.cuda.Event(enable_timing=True)
         ev.record(stream)
-        TRACE.append((label, ev))
+        TRACE.append((label, ev, time.perf_counter()))
 
 
 def tucker_host_pipelined(host, u_dt, mats_dev, codes, rows, pre, post, out_shape, cdt, dev, parts=8):

@@ -23,9 +23,11 @@ torch.cuda.synchronize()
 _pipeline._trace_on = True
 t0 = time.perf_counter()
 km.step(cache, host)
-wall = (time.perf_counter() - t0) * 1e3
+t1 = time.perf_counter()
+wall = (t1 - t0) * 1e3
 torch.cuda.synchronize()
 first = _pipeline.TRACE[0][1]
-for label, ev in _pipeline.TRACE:
-    print(f"{first.elapsed_time(ev):8.3f}  {label}")
-print(f"wall {wall:.3f} ms")
+print("  device   host-issue  event   (ms from the first event; host-issue from the call)")
+for label, ev, th in _pipeline.TRACE:
+    print(f"{first.elapsed_time(ev):8.3f}  {1e3 * (th - t0):8.3f}  {label}")
+print(f"wall {wall:.3f} ms; host time before the first event {1e3 * (_pipeline.TRACE[0][2] - t0):.3f} ms")
