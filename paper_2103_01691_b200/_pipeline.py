@@ -123,6 +123,29 @@ def tucker_host_pipelined(host, u_dt, mats_dev, codes, rows, pre, post, out_shap
     max_slab = max(sz for _, sz in slabs)
     inner = prod(dims[:last])
     u_dt = np.dtype(u_dt)
+
+    # the input copies go first: they are the critical path, so a page-locked input
+    # is queued on the copy stream before the rest of the set-up (~0.08 ms of host
+    # work).  The copy stream first waits for the compute stream, whose earlier work
+    # may still use the memory the allocator hands out here.
+    if _trace_on:
+        TRACE.clear()
+        _mark("start", compute)
+    src_all = torch.empty(host.size, dtype=dv.torch_dtype(u_dt), device=dev)
+    h_t = torch.from_numpy(host.reshape(-1, order="F"))
+    pinned_in = h_t.is_pinned()
+    s_in.wait_stream(compute)
+
+    def h2d(start, size):
+        lo, hi = inner * start, inner * (start + size)
+        ev = torch.cuda.Event()
+        with torch.cuda.stream(s_in):
+            src_all[lo:hi].copy_(h_t[lo:hi], non_blocking=pinned_in)
+            ev.record(s_in)
+            _mark(f"h2d slab {start}+{size}", s_in)
+        return ev
+
+    h2d_done = [h2d(start, size) for (start, size) in slabs] if pinned_in else None
     pre_active = [i for i in range(last) if mats_dev[i] is not None]
     has_last = mats_dev[last] is not None
 
@@ -142,7 +165,6 @@ def tucker_host_pipelined(host, u_dt, mats_dev, codes, rows, pre, post, out_shap
     def view(buf, n, npdt):
         return buf[: n * np.dtype(npdt).itemsize].view(dv.torch_dtype(npdt))
 
-    src_all = torch.empty(host.size, dtype=dv.torch_dtype(u_dt), device=dev)
     direct_mid = has_last and not pre_active and pre is None
     mid_all = None
     if has_last:
@@ -150,8 +172,6 @@ def tucker_host_pipelined(host, u_dt, mats_dev, codes, rows, pre, post, out_shap
     out_dev = torch.empty(prod(out_shape), dtype=dv.torch_dtype(cdt), device=dev)
     inner_out = prod(out_shape[:last])
 
-    h_t = torch.from_numpy(host.reshape(-1, order="F"))
-    pinned_in = h_t.is_pinned()
     host_arr = dv.pinned_host_array(out_shape, cdt)
     host_out_flat = torch.from_numpy(host_arr.reshape(-1, order="F"))
 
@@ -172,17 +192,10 @@ def tucker_host_pipelined(host, u_dt, mats_dev, codes, rows, pre, post, out_shap
                        stream_c, dev)
 
     # ---- phase 1: per input slab: H2D, pre op, directions 1..d-1
-    if _trace_on:
-        TRACE.clear()
-        _mark("start", compute)
-    for (start, size) in slabs:
+    for k, (start, size) in enumerate(slabs):
         lo, hi = inner * start, inner * (start + size)
-        ev = torch.cuda.Event()
-        with torch.cuda.stream(s_in):
-            src_all[lo:hi].copy_(h_t[lo:hi], non_blocking=pinned_in)
-            ev.record(s_in)
-            _mark(f"h2d slab {start}+{size}", s_in)
-        compute.wait_event(ev)
+        # a pageable input is copied slab by slab here (each copy blocks the host)
+        compute.wait_event(h2d_done[k] if h2d_done is not None else h2d(start, size))
         cur, cdtype = src_all[lo:hi], u_dt
         shape = list(dims[:last]) + [size]
         final_here = not has_last
