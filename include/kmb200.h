@@ -12,9 +12,14 @@
  * Conventions (all entry points):
  *   - Tensors are column-major (direction 1 fastest), as tensor.py:3-6.
  *   - Matrices L (m x n_mu) are row-major (C order), as numpy hands them over.
- *   - All pointers are DEVICE pointers; the library never allocates, never
+ *   - All pointers are DEVICE pointers; the library never allocates device
+ *     memory (every scratch buffer is caller-supplied: km_tucker's ws0/ws1,
+ *     the tcgen05 and norm workspaces, km_set_stream_workspace), never
  *     synchronises the host and launches only on `stream` (a cudaStream_t,
  *     NULL = legacy default stream).
+ *   - Per-device set-up (shared-memory opt-ins, occupancy queries, SM counts)
+ *     is cached per device id and thread safe; the CURRENT device must be the
+ *     one the pointers and the stream belong to.
  *   - Return value 0 on success, KM_EINVAL for a rejected argument, KM_ECUDA
  *     for a CUDA launch/runtime failure; km_last_error() gives the message of
  *     the last failure on the calling thread.
@@ -32,7 +37,7 @@
 extern "C" {
 #endif
 
-#define KMB200_ABI_VERSION 2
+#define KMB200_ABI_VERSION 3
 #define KM_MAX_D 8
 
 /* element types; complex values are interleaved (re, im) pairs */
@@ -75,11 +80,11 @@ typedef struct km_pointop {
 /* kernel selection (process-wide, bit flags): AUTO picks the warp-specialised
  * TMA kernels where the shape allows and balances their last wave with
  * stream-K; NO_TMA forces the cp.async kernel everywhere; NO_STREAMK keeps
- * whole tiles only (A/B testing and verification).  The stream-K tail keeps one
- * internal scratch buffer per (device, stream), allocated on first use
- * (~76 MB on 148 SMs).  Launches captured into a CUDA graph keep whole tiles:
- * the partials' publish flags are per-launch epochs, which a replayed graph
- * would repeat. */
+ * whole tiles only (A/B testing and verification).  The stream-K tail needs a
+ * scratch workspace bound to the launching stream (km_set_stream_workspace);
+ * on a stream without one the products keep whole tiles.  Launches captured
+ * into a CUDA graph keep whole tiles: the partials' publish flags are
+ * per-launch epochs, which a replayed graph would repeat. */
 enum km_kernel_policy {
   KM_POLICY_AUTO = 0,
   KM_POLICY_NO_TMA = 1,
@@ -87,6 +92,22 @@ enum km_kernel_policy {
   KM_POLICY_NO_TC_HALVES = 4  /* complex64 K' in (512, 1024] on the chunked tcgen05 kernel */
 };
 int km_set_kernel_policy(int policy);
+
+/*
+ * Stream-K scratch (partial accumulators + publish flags) of the persistent
+ * complex128/f64 TMA kernel, in the spirit of cublasSetWorkspace: the caller
+ * owns the device memory and binds it to a stream of the CURRENT device;
+ * products launched on that stream may then split their last wave of tiles
+ * over all SMs (stream-K).  km_stream_workspace_bytes gives the size for the
+ * current device (~78 MB on 148 SMs).  Binding zeroes the flags with
+ * cudaMemsetAsync on `stream`; workspace == NULL unbinds.  The workspace must
+ * stay allocated until the work queued on the stream has completed (e.g.
+ * allocate it stream-ordered on that stream).  One workspace per stream:
+ * launches on one stream are serialised, so they may share it.
+ * (No reference counterpart: tensor.py's np.matmul has no work partitioning.)
+ */
+int km_stream_workspace_bytes(size_t* bytes);
+int km_set_stream_workspace(void* stream, void* workspace, size_t bytes);
 
 /* ABI version and build info */
 int km_abi_version(void);

@@ -78,12 +78,55 @@ _raw_stream = getattr(getattr(torch, "_C", None), "_cuda_getCurrentRawStream", N
 
 def stream_ptr(dev=None):
     """The current CUDA stream of ``dev`` as a C pointer (the fast raw-stream query when
-    this torch build has it: a public ``current_stream`` lookup costs a few microseconds)."""
+    this torch build has it: a public ``current_stream`` lookup costs a few microseconds).
+
+    The first time a stream is seen, a stream-K workspace is bound to it
+    (:func:`_bind_stream_workspace`), so products launched on it may balance
+    their last wave; the library itself never allocates device memory.
+    """
+    idx = None
     if _raw_stream is not None:
         idx = torch.cuda.current_device() if dev is None else (dev.index if isinstance(dev, torch.device) else int(dev))
-        if idx is not None:
-            return ctypes.c_void_p(_raw_stream(idx))
-    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    if idx is not None:
+        raw = _raw_stream(idx)
+    else:
+        s = torch.cuda.current_stream(dev)
+        idx, raw = s.device.index, s.cuda_stream
+    if (idx, raw) not in _BOUND:
+        _bind_stream_workspace(idx, raw)
+    return ctypes.c_void_p(raw)
+
+
+_BOUND = {}  # (device index, raw stream) -> caller-owned stream-K workspace (None: not bound)
+_BOUND_MAX = 4
+
+
+def _bind_stream_workspace(idx, raw):
+    """Allocate (stream-ordered, on that stream) and bind the stream-K scratch of a stream.
+
+    At most ``_BOUND_MAX`` streams per process keep one (~78 MB each on 148 SMs); the
+    oldest binding is dropped first.  A dropped workspace is unbound before its memory
+    returns to torch's allocator, which hands it out again only in stream order.  Streams
+    being captured into a CUDA graph are not bound (graphs keep whole tiles anyway).
+    """
+    if torch.cuda.is_current_stream_capturing():
+        return
+    lib = _native.lib()
+    with torch.cuda.device(idx):
+        if len(_BOUND) >= _BOUND_MAX:
+            (oidx, oraw), _ = next(iter(_BOUND.items()))
+            with torch.cuda.device(oidx):
+                _native.check(lib.km_set_stream_workspace(ctypes.c_void_p(oraw), None, 0))
+            _BOUND.pop((oidx, oraw))
+        nbytes = ctypes.c_size_t(0)
+        _native.check(lib.km_stream_workspace_bytes(ctypes.byref(nbytes)))
+        cur = torch.cuda.current_stream(idx)
+        stream = cur if cur.cuda_stream == raw else torch.cuda.ExternalStream(raw, device=idx)
+        with torch.cuda.stream(stream):
+            ws = torch.empty(nbytes.value, dtype=torch.uint8, device=torch.device("cuda", idx))
+        _native.check(lib.km_set_stream_workspace(ctypes.c_void_p(raw), ctypes.c_void_p(ws.data_ptr()),
+                                                  nbytes.value))
+    _BOUND[(idx, raw)] = ws
 
 
 def is_fortran(t):
@@ -167,6 +210,11 @@ def upload(arr, dev):
     for the oldest one when all are busy, which bounds how far the host runs
     ahead of the device).
     """
+    return _upload(arr, dev)[0]
+
+
+def _upload(arr, dev):
+    """:func:`upload`, also returning the event of the side-stream copy (None for empty arrays)."""
     arr = np.asarray(arr)
     nbytes = arr.nbytes
     f_order = arr.ndim > 1 and arr.flags.f_contiguous and not arr.flags.c_contiguous
@@ -175,7 +223,7 @@ def upload(arr, dev):
     shape = arr.shape if not f_order else tuple(reversed(arr.shape))
     if nbytes == 0:
         out = torch.empty(shape, dtype=torch_dtype(arr.dtype), device=dev)
-        return out.permute(*reversed(range(arr.ndim))) if f_order else out
+        return (out.permute(*reversed(range(arr.ndim))) if f_order else out), None
     entry = _staging_block(nbytes)
     stage = entry[0][:nbytes]
     stage.numpy()[:] = arr.ravel(order="K").view(np.uint8)
@@ -192,7 +240,7 @@ def upload(arr, dev):
     cur.wait_event(done)
     out.record_stream(cur)
     entry[1] = done
-    return out.permute(*reversed(range(arr.ndim))) if f_order else out
+    return (out.permute(*reversed(range(arr.ndim))) if f_order else out), done
 
 
 _UPLOAD_STREAMS = {}
@@ -265,8 +313,21 @@ def pinned_host_array(shape, dtype):
         if sum(e[0].numel() for e in _PINNED_POOL) + nbytes <= _PINNED_POOL_MAX_BYTES:
             _PINNED_POOL.append(entry)
     arr = entry[0][:nbytes].numpy().view(dtype).reshape(tuple(shape), order="F")
-    entry[1] = weakref.ref(arr)
+    entry[1] = weakref.ref(_owner(arr))
     return arr
+
+
+def _owner(arr):
+    """The object at the end of ``arr``'s base chain (here the torch tensor behind ``.numpy()``).
+
+    numpy collapses view bases: ``arr[..., 0]``, ``arr.real`` or ``arr.T`` reference this
+    terminal object, not ``arr`` itself, so it is alive exactly as long as any view of the
+    buffer is.  A weakref to ``arr`` would die while such views still read the buffer.
+    """
+    base = arr
+    while isinstance(base, np.ndarray) and base.base is not None:
+        base = base.base
+    return base
 
 
 def to_host(t):
@@ -326,9 +387,15 @@ def cached_vector(v, dtype, dev):
     key = (str(dev), np.dtype(dtype).str, src.dtype.str, src.shape, src.strides, src.ctypes.data)
     hit = _VEC_CACHE.get(key)
     if hit is not None and _same_bytes(hit[0], src):
+        # the upload ran on a side stream and only the stream current at upload time waited
+        # for it: order this hit's stream after the copy too (free once it has completed)
+        if hit[2] is not None and stream_ptr(dev).value != hit[3]:
+            cur = torch.cuda.current_stream(dev)
+            cur.wait_event(hit[2])
+            hit[1].record_stream(cur)
         return hit[1]
-    t = upload(np.ascontiguousarray(src, dtype=dtype), dev)
+    t, ev = _upload(np.ascontiguousarray(src, dtype=dtype), dev)
     if hit is None and len(_VEC_CACHE) >= _VEC_CACHE_MAX:
         _VEC_CACHE.pop(next(iter(_VEC_CACHE)))
-    _VEC_CACHE[key] = (src.copy(order="K"), t)
+    _VEC_CACHE[key] = (src.copy(order="K"), t, ev, stream_ptr(dev).value)
     return t

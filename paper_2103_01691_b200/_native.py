@@ -16,7 +16,7 @@ from .errors import ConfigurationError, DeviceError, NativeLibraryError
 
 # KMB200_LIB overrides the library path (A/B builds of the same ABI)
 LIB_PATH = os.environ.get("KMB200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libkmb200.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 MAX_D = 8
 
 KM_F32, KM_F64, KM_C64, KM_C128 = 0, 1, 2, 3
@@ -43,6 +43,8 @@ EXPORTS = (
     "km_mumode_c64_tc",
     "km_norm_workspace_bytes",
     "km_norm",
+    "km_stream_workspace_bytes",
+    "km_set_stream_workspace",
 )
 
 
@@ -109,6 +111,10 @@ def _declare(lib):
     lib.km_norm.argtypes = [c_vp, c_vp, c_int, c_i64, c_int, p_op, c_vp, c_vp, c_sz, c_vp]
     lib.km_set_kernel_policy.restype = c_int
     lib.km_set_kernel_policy.argtypes = [c_int]
+    lib.km_stream_workspace_bytes.restype = c_int
+    lib.km_stream_workspace_bytes.argtypes = [ctypes.POINTER(c_sz)]
+    lib.km_set_stream_workspace.restype = c_int
+    lib.km_set_stream_workspace.argtypes = [c_vp, c_vp, c_sz]
     lib.km_pointwise.restype = c_int
     lib.km_pointwise.argtypes = [c_vp, c_vp, c_int, c_i64, p_op, c_vp]
 

@@ -118,7 +118,7 @@ def tucker_host_pipelined(host, u_dt, mats_dev, codes, rows, pre, post, out_shap
     last = d - 1
     compute = torch.cuda.current_stream(dev)
     s_in, s_out = _side_streams(dev)
-    stream_c = ctypes.c_void_p(compute.cuda_stream)
+    stream_c = dv.stream_ptr(dev)  # the compute stream (binds its stream-K workspace once)
     slabs = _input_slabs(dims[last], parts)
     max_slab = max(sz for _, sz in slabs)
     inner = prod(dims[:last])
@@ -126,15 +126,17 @@ def tucker_host_pipelined(host, u_dt, mats_dev, codes, rows, pre, post, out_shap
 
     # the input copies go first: they are the critical path, so a page-locked input
     # is queued on the copy stream before the rest of the set-up (~0.08 ms of host
-    # work).  The copy stream first waits for the compute stream, whose earlier work
-    # may still use the memory the allocator hands out here.
+    # work).  The input buffer comes from the copy stream's own allocator pool and is
+    # marked as used by the compute stream, so the copies need not wait for unrelated
+    # work the caller queued on the compute stream.
     if _trace_on:
         TRACE.clear()
         _mark("start", compute)
-    src_all = torch.empty(host.size, dtype=dv.torch_dtype(u_dt), device=dev)
+    with torch.cuda.stream(s_in):
+        src_all = torch.empty(host.size, dtype=dv.torch_dtype(u_dt), device=dev)
+    src_all.record_stream(compute)
     h_t = torch.from_numpy(host.reshape(-1, order="F"))
     pinned_in = h_t.is_pinned()
-    s_in.wait_stream(compute)
 
     def h2d(start, size):
         lo, hi = inner * start, inner * (start + size)

@@ -3,9 +3,12 @@
 // kmb200_kernels.cuh; each dtype combination is instantiated in inst_*.cu.
 #include "kmb200_launch.cuh"
 
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 
 namespace kmb {
 
@@ -13,6 +16,8 @@ extern bool g_tma_disabled;     // inst_tma_c128.cu
 extern bool g_streamk_disabled;  // inst_tma_c128.cu
 extern bool g_tc_halves_disabled;  // inst_tc32_c64.cu
 size_t tc32_workspace_bytes(int64_t m, int64_t K);  // inst_tc32_c64.cu
+size_t streamk_workspace_bytes();                    // inst_tma_c128.cu
+int bind_streamk_workspace(cudaStream_t st, void* ws, size_t bytes);  // inst_tma_c128.cu
 int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t nl, int64_t K, int64_t nr, void* ws,
                     size_t ws_bytes, cudaStream_t st);
 thread_local char g_err[512] = "";
@@ -82,15 +87,52 @@ int promote(int a, int b) {
   return c ? (d ? KM_C128 : KM_C64) : (d ? KM_F64 : KM_F32);
 }
 
-int g_num_sms = 0;
+namespace {
+std::mutex g_memo_mu;
+std::map<std::pair<int, const void*>, int> g_memo;
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+constexpr int MAX_DEVICES = 64;
+std::atomic<int> g_num_sms[MAX_DEVICES];
+}  // namespace
+
+bool memo_get(const void* key, int* value) {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lock(g_memo_mu);
+  auto it = g_memo.find({dev, key});
+  if (it == g_memo.end()) return false;
+  *value = it->second;
+  return true;
+}
+
+void memo_put(const void* key, int value) {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lock(g_memo_mu);
+  g_memo[{dev, key}] = value;
+}
+
+int ensure_smem(const void* func, int bytes, const char* what) {
+  int have = 0;
+  if (memo_get(func, &have) && have >= bytes) return KM_OK;
+  cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return fail(KM_ECUDA, "cudaFuncSetAttribute(%s): %s", what, cudaGetErrorString(e));
+  memo_put(func, bytes);
+  return KM_OK;
+}
+
 int num_sms() {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+  const int dev = current_device();
+  if (dev < 0 || dev >= MAX_DEVICES) return 148;
+  int n = g_num_sms[dev].load(std::memory_order_relaxed);
+  if (n <= 0) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+    g_num_sms[dev].store(n, std::memory_order_relaxed);
   }
-  return g_num_sms;
+  return n;
 }
 
 int pointwise_impl(const void* in, void* out, int dt, int64_t n, const km_pointop* op, cudaStream_t st);
@@ -289,6 +331,16 @@ int km_mumode_split(const void* u, int u_dtype, const void* L, int L_dtype, void
   Split sp{in_block, in_block_stride, out_block, out_block_stride};
   return mumode_impl(u, u_dtype, L, L_dtype, out, m, n_left, n_mu, n_right, nullptr,
                      static_cast<cudaStream_t>(stream), &sp);
+}
+
+int km_stream_workspace_bytes(size_t* bytes) {
+  if (!bytes) return fail(KM_EINVAL, "km_stream_workspace_bytes: NULL output");
+  *bytes = streamk_workspace_bytes();
+  return KM_OK;
+}
+
+int km_set_stream_workspace(void* stream, void* workspace, size_t bytes) {
+  return bind_streamk_workspace(static_cast<cudaStream_t>(stream), workspace, bytes);
 }
 
 int km_tc_workspace_bytes(int64_t m, int64_t n_mu, size_t* bytes) {

@@ -39,10 +39,13 @@ bool map_f32(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
 template <typename Kern>
 int launch_pairs(Kern kern, int smem, int threads, int64_t tiles, const char* what, const CUtensorMap& ahi,
                  const CUtensorMap& alo, const CUtensorMap& b, const CUtensorMap& mo, int64_t F, int m, int K,
-                 int64_t nl, cudaStream_t st, int& max_pairs) {
-  if (max_pairs == 0) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return fail(KM_ECUDA, "cudaFuncSetAttribute(%s): %s", what, cudaGetErrorString(e));
+                 int64_t nl, cudaStream_t st) {
+  // co-resident pairs, memoised per device (key: the kernel's address + 1, distinct
+  // from the shared-memory opt-in's key)
+  const void* key = reinterpret_cast<const char*>(reinterpret_cast<const void*>(kern)) + 1;
+  int max_pairs = 0;
+  if (!memo_get(key, &max_pairs)) {
+    if (int rc = ensure_smem(reinterpret_cast<const void*>(kern), smem, what)) return rc;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * (num_sms() / 2));
     cfg.blockDim = dim3(threads);
@@ -57,6 +60,7 @@ int launch_pairs(Kern kern, int smem, int threads, int64_t tiles, const char* wh
     int n = 0;
     if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) n = num_sms() / 2;
     max_pairs = n;
+    memo_put(key, n);
   }
   const int64_t pairs = tiles < max_pairs ? tiles : max_pairs;
   const cudaError_t e = launch_pdl(kern, dim3(static_cast<unsigned>(2 * pairs)), dim3(threads), smem, st, ahi, alo,
@@ -70,20 +74,17 @@ int launch(const CUtensorMap& ahi, const CUtensorMap& alo, const CUtensorMap& b,
            int m, int K, int64_t nl, bool chunked, cudaStream_t st) {
   const int64_t fib_r = KC ? F : 2 * F;
   if (chunked) {
-    static int max_pairs = 0;
     const int64_t tiles = ((2 * m + 2 * tc32k::BMR - 1) / (2 * tc32k::BMR)) * ((fib_r + tc32k::BNR - 1) / tc32k::BNR);
     return launch_pairs(mumode_tc32_chunk_kernel<KC>, tc32k::SMEM_BYTES, tc32k::THREADS, tiles,
-                        "mumode_tc32_chunk_kernel", ahi, alo, b, mo, F, m, K, nl, st, max_pairs);
+                        "mumode_tc32_chunk_kernel", ahi, alo, b, mo, F, m, K, nl, st);
   }
   const int64_t tiles = ((2 * m + 2 * tc32::BMR - 1) / (2 * tc32::BMR)) * ((fib_r + tc32::BNR - 1) / tc32::BNR);
   if ((KC ? 2 * K : K) > 512) {  // two accumulation chains of <= 512 k' per tile
-    static int max_pairs = 0;
     return launch_pairs(mumode_tc32_kernel<KC, true>, tc32::SMEM_BYTES, tc32::THREADS, tiles,
-                        "mumode_tc32_kernel (halves)", ahi, alo, b, mo, F, m, K, nl, st, max_pairs);
+                        "mumode_tc32_kernel (halves)", ahi, alo, b, mo, F, m, K, nl, st);
   }
-  static int max_pairs = 0;
   return launch_pairs(mumode_tc32_kernel<KC>, tc32::SMEM_BYTES, tc32::THREADS, tiles, "mumode_tc32_kernel", ahi,
-                      alo, b, mo, F, m, K, nl, st, max_pairs);
+                      alo, b, mo, F, m, K, nl, st);
 }
 
 }  // namespace

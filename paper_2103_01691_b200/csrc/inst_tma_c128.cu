@@ -39,36 +39,66 @@ bool make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims
   return r == CUDA_SUCCESS;
 }
 
-// Stream-K scratch, one per (device, stream): partial accumulators and flags.
-// Allocated once at the largest size a launch can need (2 * SMs stream-K
-// tiles, 2 extra pieces each), so no launch reallocates; flags start at 0 and
-// every launch publishes under a fresh epoch.
-struct SkScratch {
+// Stream-K scratch: partial accumulators and publish flags, in a caller-owned
+// device workspace bound to a stream (km_set_stream_workspace; the library
+// never allocates).  Sized for the largest launch (2 * SMs stream-K tiles, 2
+// extra pieces each); flags are zeroed at bind time and every launch publishes
+// under a fresh epoch, so consecutive launches on the stream share it safely.
+// A stream without a workspace runs whole tiles.
+struct SkBinding {
   double* part = nullptr;
   unsigned* flags = nullptr;
   unsigned epoch = 0;
 };
 
-SkScratch* sk_scratch(cudaStream_t st) {
-  static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, SkScratch> cache;
+std::mutex g_sk_mu;
+std::map<std::pair<int, cudaStream_t>, SkBinding> g_sk;
+
+size_t sk_pieces() { return static_cast<size_t>(2 * num_sms()) * 2 * tma::CONSUMERS; }
+
+}  // namespace
+
+size_t streamk_workspace_bytes() { return sk_pieces() * (2048 * sizeof(double) + sizeof(unsigned)); }
+
+int bind_streamk_workspace(cudaStream_t st, void* ws, size_t bytes) {
   int dev = 0;
   cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lock(mu);
-  SkScratch& s = cache[{dev, st}];
-  if (!s.part) {
-    const size_t pieces = static_cast<size_t>(2 * num_sms()) * 2 * tma::CONSUMERS;
-    if (cudaMalloc(&s.part, pieces * 2048 * sizeof(double)) != cudaSuccess) return nullptr;
-    if (cudaMalloc(&s.flags, pieces * sizeof(unsigned)) != cudaSuccess) return nullptr;
-    if (cudaMemset(s.flags, 0, pieces * sizeof(unsigned)) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(g_sk_mu);
+  if (!ws) {
+    g_sk.erase({dev, st});
+    return KM_OK;
   }
-  return &s;
+  const size_t need = streamk_workspace_bytes();
+  if (bytes < need)
+    return fail(KM_EINVAL, "km_set_stream_workspace: %zu bytes given, %zu needed", bytes, need);
+  if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(KM_EINVAL, "km_set_stream_workspace: workspace not 256-B aligned");
+  SkBinding b;
+  b.part = static_cast<double*>(ws);
+  b.flags = reinterpret_cast<unsigned*>(b.part + sk_pieces() * 2048);
+  const cudaError_t e = cudaMemsetAsync(b.flags, 0, sk_pieces() * sizeof(unsigned), st);
+  if (e != cudaSuccess) return fail(KM_ECUDA, "km_set_stream_workspace: %s", cudaGetErrorString(e));
+  g_sk[{dev, st}] = b;
+  return KM_OK;
+}
+
+namespace {
+
+// the bound scratch of (current device, st) with a fresh epoch; false when none is bound
+bool sk_scratch(cudaStream_t st, double** part, unsigned** flags, unsigned* epoch) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(g_sk_mu);
+  auto it = g_sk.find({dev, st});
+  if (it == g_sk.end()) return false;
+  *part = it->second.part;
+  *flags = it->second.flags;
+  *epoch = ++it->second.epoch;
+  return true;
 }
 
 template <typename Kern>
 int set_smem(Kern k) {
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tma::SMEM_BYTES);
-  return e == cudaSuccess ? KM_OK : fail(KM_ECUDA, "cudaFuncSetAttribute(tma): %s", cudaGetErrorString(e));
+  return ensure_smem(reinterpret_cast<const void*>(k), tma::SMEM_BYTES, "mumode_tma_kernel");
 }
 
 // Stream-K launch of a product (any real / complex mix).  Returns -1 when the
@@ -107,17 +137,9 @@ int launch_streamk(const CUtensorMap& ma, const CUtensorMap& mb, void* out, int6
   sk.iters = (tiles - sk.sk_base) * KT;
   const int64_t per = sk.iters / S;  // >= KT (tiles > S: a tile spans at most 2 CTAs) or >= KT/2
   sk.slots = static_cast<int>((KT + per - 1) / per);
-  SkScratch* scr = sk_scratch(st);
-  if (!scr) return -1;
+  if (!sk_scratch(st, &sk.part, &sk.flags, &sk.epoch)) return -1;
   auto kern = mumode_tma_kernel<KC, OPK, CL, CU, true>;
-  static bool attr = false;
-  if (!attr) {
-    if (int rc = set_smem(kern)) return rc;
-    attr = true;
-  }
-  sk.part = scr->part;
-  sk.flags = scr->flags;
-  sk.epoch = ++scr->epoch;
+  if (int rc = set_smem(kern)) return rc;
   TO* outp = static_cast<TO*>(out);
   void* args[] = {const_cast<CUtensorMap*>(&ma), const_cast<CUtensorMap*>(&mb), &outp, &M, &N, &K, &nl,
                   const_cast<OpDev*>(&op), const_cast<Split*>(&sp), &sk};
@@ -135,11 +157,7 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* out, int64_t M, i
     if (rc >= 0) return rc;
   }
   auto kern = mumode_tma_kernel<KC, OPK, CL, CU, false>;
-  static bool attr = false;
-  if (!attr) {
-    if (int rc = set_smem(kern)) return rc;
-    attr = true;
-  }
+  if (int rc = set_smem(kern)) return rc;
   const int64_t tiles = ((M + tma::BM - 1) / tma::BM) * ((N + tma::BN - 1) / tma::BN);
   const int64_t S = num_sms();
   StreamK none;

@@ -15,12 +15,7 @@ int launch_cfg(const void* u, const void* L, void* out, int64_t M, int N, int K,
   constexpr int BM = WT_ * WM_, BN = WT_ * WN_;
   using Lay = SmemLayout<TU, TL, KC, BM, BN>;
   auto kern = mumode_kernel<S, CU, CL, KC, OPK, WM_, WN_, WT_>;
-  static bool attr_set = false;  // once per instantiation and process
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL);
-    if (e != cudaSuccess) return fail(KM_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    attr_set = true;
-  }
+  if (int rc = ensure_smem(reinterpret_cast<const void*>(kern), Lay::TOTAL, "mumode_kernel")) return rc;
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   if (tiles > 0x7fffffffLL) return fail(KM_EINVAL, "km_mumode: %lld tiles exceed the grid limit", (long long)tiles);
   const cudaError_t e = launch_pdl(kern, dim3(static_cast<unsigned>(tiles)), dim3(32 * WM_ * WN_), Lay::TOTAL, st,

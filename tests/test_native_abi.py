@@ -130,3 +130,40 @@ def test_tucker_buffer_rules_checked_before_launch():
     for ws0, ws1 in ((u, w1), (w0, u), (w0, out), (w0, w0)):
         rc = lib.km_tucker(u, _native.KM_C128, d, dims, mats, codes, rows, out, ws0, ws1, None, None, None)
         assert rc == _native.KM_EINVAL and b"aliases" in lib.km_last_error()
+
+
+def test_library_sources_never_allocate_device_memory():
+    """kmb200.h promises the library never allocates device memory: every scratch buffer
+    (km_tucker's workspaces, the tcgen05 planes, the norm partials, the stream-K scratch)
+    is caller-supplied.  No allocation call may appear in the library's sources."""
+    csrc = os.path.join(ROOT, "paper_2103_01691_b200", "csrc")
+    banned = re.compile(r"\b(cudaMalloc\w*|cuMemAlloc\w*|cudaHostAlloc|cudaMallocHost|cuMemCreate)\s*\(")
+    for name in sorted(os.listdir(csrc)):
+        if name.endswith((".cu", ".cuh", ".h")):
+            text = open(os.path.join(csrc, name)).read()
+            assert not banned.search(text), f"{name} allocates device memory"
+
+
+def test_per_device_state_has_no_process_wide_flags():
+    """Set-up the library caches per device (smem opt-ins, cluster occupancy, SM counts) is
+    keyed by the device id (memo_get/memo_put, ensure_smem); a process-wide `static bool` or
+    `static int` flag would skip the set-up on a second device."""
+    csrc = os.path.join(ROOT, "paper_2103_01691_b200", "csrc")
+    bad = re.compile(r"static\s+(bool|int)\s+(attr\w*|max_pairs|g_num_sms)\b")
+    for name in sorted(os.listdir(csrc)):
+        if name.endswith((".cu", ".cuh")):
+            assert not bad.search(open(os.path.join(csrc, name)).read()), name
+
+
+def test_stream_workspace_entry_points():
+    lib = _native.lib()
+    nb = ctypes.c_size_t()
+    if not HAS_CUDA:
+        # the size depends on the device's SM count; without a device it still answers
+        assert lib.km_stream_workspace_bytes(ctypes.byref(nb)) == 0 and nb.value > 0
+    assert lib.km_stream_workspace_bytes(None) == _native.KM_EINVAL
+    # too small a workspace is rejected before anything is queued
+    rc = lib.km_set_stream_workspace(None, ctypes.c_void_p(0x1000), 16)
+    assert rc == _native.KM_EINVAL and b"needed" in lib.km_last_error()
+    # unbinding a stream that has no workspace is a no-op
+    assert lib.km_set_stream_workspace(None, None, 0) == 0
