@@ -12,14 +12,17 @@ complex multiply-add.  Prints ONE JSON line (rank 0).
 * e2e        — the same metric through the public drop-in call
                ``km.step(cache, u_host)`` with a pinned host array in and a host
                array out (H2D + D2H inside the timed region).
-* roofline   — the dominant kernel (mumode_kernel, DMMA) achieved TFLOP/s vs
+* roofline   — the dominant kernel (mumode_tma_kernel, DMMA) achieved TFLOP/s vs
                the measured FP64 tensor-core peak (profiles/fp64_peak.json).
 * cpu_baseline — the reference algorithm (oracle/ numpy restatement, same
                numpy.matmul calls as tensor.py:124-139) on the host cores.
 
 The state (268 MB) exceeds the 126 MB L2, so no flush is needed between steps.
-Multi-GPU (torchrun, N>1): the 256^3 state is split into slabs along
-direction 3 (strong scaling); see paper_2103_01691_b200/dist.py.
+Multi-GPU (N>1): the 256^3 state is split into slabs along direction 3
+(strong scaling); see paper_2103_01691_b200/dist.py.  Launched either by the
+driver's torchrun or, for ``--gpus N`` without a torchrun environment, by
+bench.py itself (one rank per GPU on 127.0.0.1); ``n_gpus`` is the world size
+the ranks actually formed, in both arms.
 """
 
 from __future__ import annotations
@@ -174,6 +177,7 @@ def cpu_reference(u, cache, budget_s, max_steps):
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     u, cache = build_inputs()
@@ -185,7 +189,7 @@ def run_reference(args):
         "metric": METRIC,
         "value": cb["value"],
         "unit": "steps/s",
-        "n_gpus": args.gpus,
+        "n_gpus": world,
         "steps": steps,
         "warmup": args.warmup,
         "ms_per_step": cb["ms_per_step"],
@@ -195,6 +199,7 @@ def run_reference(args):
         "dtype": "complex128",
         "data": "synthetic (seeded normal complex tensor)",
         "config": dict(WORKLOAD),
+        "parallelism": "CPU reference (host cores of rank 0)",
         "gflops": cb["gflops"],
         "cpu_baseline": cb,
         "e2e": {"value": cb["value"], "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -353,7 +358,7 @@ def run_ours(args):
             e2e = {"value": None, "unit": "steps/s", "error": f"{type(exc).__name__}: {exc}"}
 
     if rank == 0:
-        cb = cpu_reference(u_host, cache, budget_s=20.0, max_steps=50) if (world == 1 and not args.no_cpu) else None
+        cb = cpu_reference(u_host, cache, budget_s=20.0, max_steps=50) if not args.no_cpu else None
         line = {
             "metric": METRIC,
             "value": value,
@@ -367,8 +372,9 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "complex128",
             "data": "synthetic (seeded normal complex tensor, host-built expm factors)",
-            "config": dict(WORKLOAD, parallelism=("single GPU" if not slab else
-                                                  f"slab{world} along direction 3, {args.exchange} exchange")),
+            "config": dict(WORKLOAD),
+            "parallelism": ("single GPU" if not slab else
+                            f"slab{world} along direction 3, {args.exchange} exchange"),
             "gflops": value * FLOP_PER_STEP / 1e9,
             "roofline": roof,
             "cpu_baseline": cb,
@@ -383,6 +389,46 @@ def run_ours(args):
         tdist.destroy_process_group()
 
 
+def launch_ranks(args, argv):
+    """``--gpus N`` (N > 1) without a torchrun environment: start the N ranks ourselves.
+
+    Runs ``python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1``
+    on this same script and arguments (one process per GPU, rank = local GPU), after
+    checking that N GPUs are visible, and returns its exit code; rank 0 prints the JSON
+    line.  ``KMB200_BENCH_SELFTEST=1`` skips the GPU check (the CPU launcher test).
+    """
+    selftest = os.environ.get("KMB200_BENCH_SELFTEST") == "1"
+    if not selftest:
+        import torch
+
+        have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}", file=sys.stderr)
+            return 2
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + argv
+    return subprocess.run(cmd).returncode
+
+
+def selftest_rank(args):
+    """KMB200_BENCH_SELFTEST=1 under the launcher: gloo rendezvous only, rank 0 reports the world."""
+    import torch
+    import torch.distributed as tdist
+
+    tdist.init_process_group("gloo")
+    t = torch.tensor([1.0])
+    tdist.all_reduce(t)
+    if tdist.get_rank() == 0:
+        print(json.dumps({"impl": args.impl, "n_gpus": tdist.get_world_size(), "ranks_seen": int(t.item()),
+                          "selftest": True}), flush=True)
+    tdist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -393,7 +439,21 @@ def main():
     ap.add_argument("--slab", action="store_true", help="run the multi-GPU slab path even on one rank (testing)")
     ap.add_argument("--exchange", choices=["nccl", "peer"], default="nccl",
                     help="multi-GPU all-to-all: NCCL, or fused into the products via NVLink peer stores")
+    argv = sys.argv[1:]
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(args, argv))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
+    if os.environ.get("KMB200_BENCH_SELFTEST") == "1":
+        selftest_rank(args)
+        return
+    if world > 1 and args.impl == "ours":
+        # communicator lines (nranks) for the driver's check; INIT only, so the JSON line stays last
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if args.impl == "reference":
         run_reference(args)
     else:
