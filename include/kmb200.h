@@ -242,6 +242,16 @@ int km_tucker_workspace(int u_dtype, int d, const int64_t* dims, const void* con
 int km_pointwise(const void* in, void* out, int dtype, int64_t n, const km_pointop* op,
                  void* stream);
 
+/* km_pointwise with a widening store: in_dtype KM_C64 -> out_dtype KM_C128
+ * (or equal dtypes; not in place when widening).  The op is evaluated as
+ * numpy evaluates it on a state of in_dtype: for a complex64 state the GPE
+ * density's squares and sum are float32 operations (psi.real**2 +
+ * psi.imag**2, problems.py:543) before the float64 division by the weight
+ * product, and the result is complex128 (the complex128 phase factor
+ * promotes it, problems.py:545).  op == NULL / KM_OP_NONE is a plain cast. */
+int km_pointwise_cast(const void* in, int in_dtype, void* out, int out_dtype, int64_t n,
+                      const km_pointop* op, void* stream);
+
 /*
  * Norms of a - b (b may be NULL) over n elements, result written to the
  * device double *result (reference: tensor.norm, tensor.py:169-198, and

@@ -38,6 +38,7 @@ EXPORTS = (
     "km_tucker",
     "km_tucker_workspace",
     "km_pointwise",
+    "km_pointwise_cast",
     "km_set_kernel_policy",
     "km_tc_workspace_bytes",
     "km_mumode_c64_tc",
@@ -117,6 +118,8 @@ def _declare(lib):
     lib.km_set_stream_workspace.argtypes = [c_vp, c_vp, c_sz]
     lib.km_pointwise.restype = c_int
     lib.km_pointwise.argtypes = [c_vp, c_vp, c_int, c_i64, p_op, c_vp]
+    lib.km_pointwise_cast.restype = c_int
+    lib.km_pointwise_cast.argtypes = [c_vp, c_int, c_vp, c_int, c_i64, p_op, c_vp]
 
 
 def lib():

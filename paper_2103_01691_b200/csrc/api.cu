@@ -3,6 +3,7 @@
 // kmb200_kernels.cuh; each dtype combination is instantiated in inst_*.cu.
 #include "kmb200_launch.cuh"
 
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -197,7 +198,14 @@ int mumode_impl(const void* u, int udt, const void* L, int ldt, void* out, int64
   return pointwise_impl(out, out, promote(udt, ldt), M * N, post, st);
 }
 
-template <typename T>
+// complex64 -> complex128, exact
+__global__ void widen_kernel(const float2* __restrict__ in, double2* __restrict__ out, int64_t n) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[p] = widen(in[p]);
+}
+
+template <typename TI, typename TO>
 int pointwise_t(const void* in, void* out, int64_t n, const OpDev& op, cudaStream_t st) {
   const int threads = 256;
   int64_t blocks = (n + threads - 1) / threads;
@@ -218,28 +226,50 @@ int pointwise_t(const void* in, void* out, int64_t n, const OpDev& op, cudaStrea
     grid = dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by));
   }
   if (op.kind == KM_OP_GPE_PHASE)
-    pointwise_kernel<T, KM_OP_GPE_PHASE><<<grid, threads, 0, st>>>(static_cast<const T*>(in), static_cast<T*>(out),
-                                                                    n, op);
+    pointwise_kernel<TI, TO, KM_OP_GPE_PHASE><<<grid, threads, 0, st>>>(static_cast<const TI*>(in),
+                                                                         static_cast<TO*>(out), n, op);
   else
-    pointwise_kernel<T, KM_OP_DIAG><<<grid, threads, 0, st>>>(static_cast<const T*>(in), static_cast<T*>(out), n, op);
+    pointwise_kernel<TI, TO, KM_OP_DIAG><<<grid, threads, 0, st>>>(static_cast<const TI*>(in), static_cast<TO*>(out),
+                                                                    n, op);
   return check_launch("pointwise_kernel");
 }
 
-int pointwise_impl(const void* in, void* out, int dt, int64_t n, const km_pointop* op, cudaStream_t st) {
-  if (!is_complex(dt)) return fail(KM_EINVAL, "km_pointwise: dtype %d is not complex", dt);
-  if (!op || op->kind == KM_OP_NONE) {
+int pointwise_cast_impl(const void* in, int idt, void* out, int odt, int64_t n, const km_pointop* op,
+                        cudaStream_t st) {
+  if (!is_complex(idt) || !is_complex(odt))
+    return fail(KM_EINVAL, "km_pointwise: dtypes %d -> %d are not complex", idt, odt);
+  if (idt == KM_C128 && odt == KM_C64)
+    return fail(KM_EINVAL, "km_pointwise: complex128 -> complex64 would round the state");
+  if (idt != odt && in == out) return fail(KM_EINVAL, "km_pointwise: a widening pass cannot run in place");
+  if ((!op || op->kind == KM_OP_NONE) && idt == odt) {
     if (in != out && n > 0) {
-      cudaError_t e = cudaMemcpyAsync(out, in, n * elem_bytes(dt), cudaMemcpyDeviceToDevice, st);
+      cudaError_t e = cudaMemcpyAsync(out, in, n * elem_bytes(idt), cudaMemcpyDeviceToDevice, st);
       if (e != cudaSuccess) return fail(KM_ECUDA, "km_pointwise copy: %s", cudaGetErrorString(e));
     }
     return KM_OK;
   }
-  int rc = validate_op(op, "km_pointwise");
-  if (rc) return rc;
+  if (!op || op->kind == KM_OP_NONE) {  // plain widening
+    op = nullptr;
+  } else {
+    int rc = validate_op(op, "km_pointwise");
+    if (rc) return rc;
+  }
   if (n <= 0) return KM_OK;
+  if (!op) {
+    if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 7)
+      return fail(KM_EINVAL, "km_pointwise: misaligned buffers");
+    widen_kernel<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 8 * num_sms())), 256, 0, st>>>(
+        static_cast<const float2*>(in), static_cast<double2*>(out), n);
+    return check_launch("widen_kernel");
+  }
   const OpDev o = to_dev(op);
-  if (dt == KM_C128) return pointwise_t<double2>(in, out, n, o, st);
-  return pointwise_t<float2>(in, out, n, o, st);
+  if (idt == KM_C128) return pointwise_t<double2, double2>(in, out, n, o, st);
+  if (odt == KM_C128) return pointwise_t<float2, double2>(in, out, n, o, st);
+  return pointwise_t<float2, float2>(in, out, n, o, st);
+}
+
+int pointwise_impl(const void* in, void* out, int dt, int64_t n, const km_pointop* op, cudaStream_t st) {
+  return pointwise_cast_impl(in, dt, out, dt, n, op, st);
 }
 
 int tucker_plan(int udt, int d, const int64_t* dims, const void* const* mats, const int* mdt, const int64_t* rows,
@@ -381,6 +411,11 @@ int km_tucker_workspace(int u_dtype, int d, const int64_t* dims, const void* con
 
 int km_pointwise(const void* in, void* out, int dtype, int64_t n, const km_pointop* op, void* stream) {
   return pointwise_impl(in, out, dtype, n, op, static_cast<cudaStream_t>(stream));
+}
+
+int km_pointwise_cast(const void* in, int in_dtype, void* out, int out_dtype, int64_t n, const km_pointop* op,
+                      void* stream) {
+  return pointwise_cast_impl(in, in_dtype, out, out_dtype, n, op, static_cast<cudaStream_t>(stream));
 }
 
 int km_tucker(const void* u, int u_dtype, int d, const int64_t* dims, const void* const* mats,

@@ -22,6 +22,7 @@ The host helpers (grids, initial states) follow problems.py:273-292,
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 
@@ -103,6 +104,23 @@ def _strang_dtype(psi_dtype, cache):
     return np.result_type(psi_dtype, np.complex128, *cache.exp_dtypes())
 
 
+def _opening_phase_widened(state, op, dev):
+    """The opening half-phase of a complex64 state, stored as complex128 (km_pointwise_cast).
+
+    The reference forms the density of a complex64 state in float32
+    (``psi.real**2 + psi.imag**2`` on float32 arrays, problems.py:543) and the
+    complex128 phase factor promotes the product to complex128 (problems.py:545);
+    converting to complex128 first would form the density in float64 instead.
+    Returns a column-major complex128 device tensor.
+    """
+    t = state if dv.is_tensor(state) and state.is_cuda else dv.to_device(np.asarray(state), np.complex64, dev)
+    t = dv.tensor_as(t, np.complex64)
+    out = dv.fortran_empty(tuple(t.shape), dv.torch.complex128, dev)
+    _native.check(_native.lib().km_pointwise_cast(t.data_ptr(), _native.KM_C64, out.data_ptr(), _native.KM_C128,
+                                                  t.numel(), ctypes.byref(op), dv.stream_ptr(dev)))
+    return out
+
+
 def gpe_strang_step(linear_cache, weights, psi, tau, _timer=None):
     """One Strang step in the weighted variables (problems.py:548-565).
 
@@ -127,15 +145,29 @@ def gpe_strang_step(linear_cache, weights, psi, tau, _timer=None):
     pre = _gpe_op(po.shape, w_dev, half_tau, inner_dev)
     post = _gpe_op(po.shape, w_dev, half_tau, inner_dev)
     state = po.obj
-    if po.dtype != out_dtype and not po.is_tensor:
+    host_in = not (po.is_tensor and po.obj.is_cuda)
+    if po.dtype == np.complex64 and out_dtype == np.complex128:
+        # float32 density in the opening phase, then the complex128 step (see _opening_phase_widened)
+        state = _opening_phase_widened(state, pre, dev)
+        pre = None
+    elif po.dtype != out_dtype and not po.is_tensor:
         state = np.asarray(state).astype(out_dtype, order="F")
     elif po.is_tensor and dv.np_dtype(state.dtype) != out_dtype:
         state = dv.tensor_as(state, out_dtype)
     mats = _cache_mats(linear_cache, _Operand(state))
+
+    def run():
+        res = run_tucker(state, mats, pre=pre, post=post, out_dtype=out_dtype, keepalive=w_dev)
+        if host_in and dv.is_tensor(res) and not (po.is_tensor and not po.obj.is_cuda):
+            return dv.to_host(res)
+        if host_in and dv.is_tensor(res):  # CPU torch tensor in -> CPU torch tensor out
+            return dv.torch.from_numpy(dv.to_host(res))
+        return res
+
     if _timer is not None:
         with _timer.mode_products():
-            return run_tucker(state, mats, pre=pre, post=post, out_dtype=out_dtype, keepalive=w_dev)
-    return run_tucker(state, mats, pre=pre, post=post, out_dtype=out_dtype, keepalive=w_dev)
+            return run()
+    return run()
 
 
 def gpe_strang_run(linear_cache, weights, psi, tau, steps):
@@ -163,11 +195,16 @@ def gpe_strang_run(linear_cache, weights, psi, tau, steps):
     half_tau = 0.5 * tau
     single = _gpe_op(po.shape, w_dev, half_tau, inner_dev, 1)
     double = _gpe_op(po.shape, w_dev, half_tau, inner_dev, 2)
-    state = po.obj if po.is_tensor and po.obj.is_cuda else dv.to_device(np.asarray(po.obj), out_dtype, dev)
-    state = dv.tensor_as(state, out_dtype)
+    opened = False
+    if po.dtype == np.complex64 and out_dtype == np.complex128:
+        state = _opening_phase_widened(po.obj, single, dev)  # float32 density, as the reference
+        opened = True
+    else:
+        state = po.obj if po.is_tensor and po.obj.is_cuda else dv.to_device(np.asarray(po.obj), out_dtype, dev)
+        state = dv.tensor_as(state, out_dtype)
     mats = _cache_mats(linear_cache, _Operand(state))
     for k in range(steps):
-        pre = single if k == 0 else None
+        pre = single if (k == 0 and not opened) else None
         post = single if k == steps - 1 else double
         state = run_tucker(state, mats, pre=pre, post=post, out_dtype=out_dtype, keepalive=keep)
     if po.is_tensor and po.obj.is_cuda:

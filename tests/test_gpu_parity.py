@@ -116,8 +116,10 @@ def test_gpe_strang_golden():
     assert rel(p, g["gpe16__out5"]) <= 1e-12
     c64 = km.PropagatorCache(0.1, tuple(e.astype(np.complex64) for e in cache.exps))
     p64 = km.gpe_strang_step(c64, ws, g["gpe16__psi0"].astype(np.complex64), 0.1)
-    assert p64.dtype == g["gpe16c64__out1"].dtype
-    assert rel(p64, g["gpe16c64__out1"]) <= 1e-5
+    assert p64.dtype == g["gpe16c64__out1"].dtype == np.complex128
+    # the reference promotes the state to complex128 in the opening phase (with a float32
+    # density, problems.py:543-545), so the complex128 bar applies
+    assert rel(p64, g["gpe16c64__out1"]) <= 1e-12
 
 
 # ------------------------------------------------ reference test semantics
