@@ -175,15 +175,32 @@ class SlabStepper:
         mats = cache.device_exps((np.complex128,) * 3, dev)
         return cls(plan, rank, dv.as_fortran(local).permute(2, 1, 0).reshape(-1), mats, NcclExchange(group))
 
-    def _run(self, calls, src, dst_final, scratch):
+    def _run(self, calls, src, dst_final, scratch, post=None):
+        """The products of one schedule half; ``post`` (a local-layout km_pointop of the layout
+        the last product writes) is fused into that product's epilogue when its layout is
+        plain and its direction is the last one, else applied as an in-place pass after it."""
         stream = dv.stream_ptr(self.a.device)
         cur = src
         for idx, (mu, m, nl, nmu, nr, kcb, kbs, ncb, nbs) in enumerate(calls):
-            dst = dst_final if idx == len(calls) - 1 else scratch
-            _native.check(self.lib.km_mumode_split(
-                cur.data_ptr(), self.code, self.mats[mu].data_ptr(), self.mcodes[mu], dst.data_ptr(),
-                m, nl, nmu, nr, kcb, kbs, ncb, nbs, stream))
+            last = idx == len(calls) - 1
+            dst = dst_final if last else scratch
+            if last and post is not None and kcb == nmu and ncb == m and mu == len(self.plan.dims) - 1:
+                _native.check(self.lib.km_mumode(
+                    cur.data_ptr(), self.code, self.mats[mu].data_ptr(), self.mcodes[mu], dst.data_ptr(),
+                    m, nl, nmu, nr, ctypes.byref(post), stream))
+                post = None
+            else:
+                _native.check(self.lib.km_mumode_split(
+                    cur.data_ptr(), self.code, self.mats[mu].data_ptr(), self.mcodes[mu], dst.data_ptr(),
+                    m, nl, nmu, nr, kcb, kbs, ncb, nbs, stream))
             cur = dst
+        if post is not None:
+            self._phase(dst_final, post)
+
+    def _phase(self, buf, op):
+        """In-place standalone pointwise pass over the local slab."""
+        _native.check(self.lib.km_pointwise(buf.data_ptr(), buf.data_ptr(), self.code, self.plan.local,
+                                            ctypes.byref(op), dv.stream_ptr(self.a.device)))
 
     def pre_exchange(self):
         before, _ = self.plan.even_calls() if self.layout == "A" else self.plan.odd_calls()
@@ -195,10 +212,18 @@ class SlabStepper:
         self._run(after, self.recv, self.a, self.w)
         self.layout = "B" if self.layout == "A" else "A"
 
-    def step(self):
-        self.pre_exchange()
-        self.comm.exchange(self.recv, self.send)
+    def begin_step(self, **kw):
+        """Everything of one step before its exchange; returns the send buffer."""
+        return self.pre_exchange()
+
+    def end_step(self, **kw):
+        """Everything of one step after its exchange."""
         self.post_exchange()
+
+    def step(self, **kw):
+        self.begin_step(**kw)
+        self.comm.exchange(self.recv, self.send)
+        self.end_step(**kw)
 
     def local_state(self):
         """The local slab as a column-major (n1, n2, c3) [layout A] or (n1, c2, n3) [layout B] tensor view."""
@@ -207,6 +232,126 @@ class SlabStepper:
 
     def time_launches(self, reps=10):  # pragma: no cover - per-launch timing lives in LocalStepper
         return None
+
+
+class SlabGpeStepper(SlabStepper):
+    """Gross–Pitaevskii Strang steps (problems.py:548-565) of a 3D slab-decomposed state.
+
+    Configuration 5 over P GPUs.  The nonlinear half-phase
+    ``psi * exp(i coef (1 - |psi|^2 / w))`` is pointwise, so it runs on whichever
+    layout the slab is in: its weight product ``w1[i1]*w2[i2]*w3[i3]`` is the
+    global one seen through slab offsets (layout A: ``w3 + r*c3``; layout B:
+    ``w2 + r*c2`` and the inner product ``(w1*w2)`` from row ``n1*r*c2``), so
+    every element gets exactly the factors (and rounding) of the single-GPU step.
+    As in :func:`problems.gpe_strang_run`, the closing half-phase of step k and
+    the opening one of step k+1 are one ``repeat = 2`` rotation: fused into the
+    direction-3 product's epilogue after even steps (that product writes layout
+    B unblocked), a standalone in-place pass after odd steps (their last
+    product writes layout A through the blocked input).  ``run(steps)`` (or
+    ``begin_step(k=, steps=)`` / ``end_step(k=, steps=)`` around the exchange)
+    applies the single opening and closing phases at the ends.
+    """
+
+    def __init__(self, plan, rank, local_a, mats, comm, weights_dev, inner_dev, half_tau):
+        super().__init__(plan, rank, local_a, mats, comm)
+        self.wdev = list(weights_dev)
+        self.inner = inner_dev
+        self.coef = 0.5 * half_tau  # problems.py:545
+        self.launches_per_step = 4
+
+    def _op(self, layout, repeat):
+        n1, n2, n3 = self.plan.dims
+        c2, c3, r = self.plan.c2, self.plan.c3, self.rank
+        op = _native.PointOp()
+        op.kind = _native.OP_GPE_PHASE
+        op.d = 3
+        op.repeat = repeat
+        op.coef = self.coef
+        w = [t.data_ptr() for t in self.wdev]
+        if layout == "A":
+            dims, w[2], inner = (n1, n2, c3), w[2] + 8 * r * c3, self.inner.data_ptr()
+        else:
+            dims, w[1], inner = (n1, c2, n3), w[1] + 8 * r * c2, self.inner.data_ptr() + 8 * n1 * r * c2
+        for i in range(3):
+            op.dims[i] = dims[i]
+            op.weights[i] = w[i]
+        op.inner_weights = inner
+        return op
+
+    def begin_step(self, k=0, steps=1, **kw):
+        if k == 0:
+            self._phase(self.a, self._op(self.layout, 1))
+        return self.pre_exchange()
+
+    def end_step(self, k=0, steps=1, **kw):
+        _, after = self.plan.even_calls() if self.layout == "A" else self.plan.odd_calls()
+        out_layout = "B" if self.layout == "A" else "A"
+        self._run(after, self.recv, self.a, self.w, post=self._op(out_layout, 1 if k == steps - 1 else 2))
+        self.layout = out_layout
+
+    def run(self, steps):
+        for k in range(steps):
+            self.step(k=k, steps=steps)
+
+    @classmethod
+    def from_global(cls, u_host, cache, weights, tau, dev, group=None):
+        import torch.distributed as tdist
+
+        from .tensor import inner_weight_product
+
+        rank, P = tdist.get_rank(group), tdist.get_world_size(group)
+        plan = SlabPlan(u_host.shape, P)
+        local = dv.to_device(np.asfortranarray(plan.slab_a(u_host, rank)), np.complex128, dev)
+        mats = cache.device_exps((np.complex128,) * 3, dev)
+        w_dev = [dv.cached_vector(w, np.float64, dev) for w in weights]
+        inner = dv.cached_vector(inner_weight_product(weights, u_host.shape), np.float64, dev)
+        return cls(plan, rank, dv.as_fortran(local).permute(2, 1, 0).reshape(-1), mats, NcclExchange(group),
+                   w_dev, inner, 0.5 * tau)
+
+
+class SlabTdpotStepper(SlabStepper):
+    """Configuration 4 over P GPUs: time-dependent-potential Strang steps of a slab state.
+
+    The potential flows ``exp(-i x3 ∫ sin^2)`` over the two half steps are
+    diagonal along direction 3 and commute with the other directions'
+    products, so each rank folds them into its copy of E3 at the start of
+    every step (``km_diag_phase_fold`` from the node vector and two scalars,
+    as :func:`problems.tdpot_strang_step` does on one GPU) and the step is the
+    plain slab step, one exchange per step.  ``begin_step(t=, tau=)``.
+    """
+
+    def __init__(self, plan, rank, local_a, mats, comm, x_nodes_dev):
+        super().__init__(plan, rank, local_a, mats, comm)
+        self.e3 = self.mats[2]
+        self.folded = dv.torch.empty_like(self.e3)
+        self.x = x_nodes_dev
+        self.launches_per_step = 4
+
+    def begin_step(self, t=0.0, tau=0.0, **kw):
+        from .problems import sin2_integral
+
+        c_a, c_b = sin2_integral(t, t + 0.5 * tau), sin2_integral(t + 0.5 * tau, t + tau)
+        m, k = self.e3.shape
+        _native.check(self.lib.km_diag_phase_fold(self.e3.data_ptr(), self.folded.data_ptr(), m, k,
+                                                  self.x.data_ptr(), self.x.data_ptr(), c_a, c_b,
+                                                  dv.stream_ptr(self.a.device)))
+        self.mats[2] = self.folded
+        return self.pre_exchange()
+
+    def run(self, t0, tau, steps):
+        for s_ in range(steps):
+            self.step(t=t0 + s_ * tau, tau=tau)
+
+    @classmethod
+    def from_global(cls, u_host, cache, x_nodes, dev, group=None):
+        import torch.distributed as tdist
+
+        rank, P = tdist.get_rank(group), tdist.get_world_size(group)
+        plan = SlabPlan(u_host.shape, P)
+        local = dv.to_device(np.asfortranarray(plan.slab_a(u_host, rank)), np.complex128, dev)
+        mats = cache.device_exps((np.complex128,) * 3, dev)
+        x = dv.cached_vector(np.asarray(x_nodes, dtype=float), np.float64, dev)
+        return cls(plan, rank, dv.as_fortran(local).permute(2, 1, 0).reshape(-1), mats, NcclExchange(group), x)
 
 
 class PeerSlabStepper(SlabStepper):
@@ -299,7 +444,10 @@ class VirtualSlabGroup:
     while nothing waits on another process (SURVEY §4 "virtual-rank" test).
     """
 
-    def __init__(self, u_host, cache, dev, P, exchange="nccl"):
+    def __init__(self, u_host, cache, dev, P, exchange="nccl", kind="plain", weights=None, tau=None,
+                 x_nodes=None):
+        """``kind``: "plain" (exact steps), "gpe" (SlabGpeStepper: ``weights``, ``tau``) or
+        "tdpot" (SlabTdpotStepper: ``x_nodes``)."""
         self.plan = SlabPlan(u_host.shape, P)
         self.exchange = exchange
         mats = cache.device_exps((np.complex128,) * 3, dev)
@@ -309,15 +457,29 @@ class VirtualSlabGroup:
             local = dv.to_device(np.asfortranarray(self.plan.slab_a(u_host, r)), np.complex128, dev)
             locals_.append(local.permute(2, 1, 0).reshape(-1))
         if exchange == "peer":
+            if kind != "plain":
+                raise ValueError("the peer exchange steps plain propagators only")
             recv = [(dv.torch.empty_like(x), dv.torch.empty_like(x)) for x in locals_]
             ptrs = [[recv[s][k].data_ptr() for s in range(P)] for k in range(2)]
             for r in range(P):
                 self.ranks.append(PeerSlabStepper(self.plan, r, locals_[r], mats, recv[r], ptrs, lambda: None))
+        elif kind == "gpe":
+            from .tensor import inner_weight_product
+
+            w_dev = [dv.cached_vector(w, np.float64, dev) for w in weights]
+            inner = dv.cached_vector(inner_weight_product(weights, u_host.shape), np.float64, dev)
+            for r in range(P):
+                self.ranks.append(SlabGpeStepper(self.plan, r, locals_[r], list(mats), None, w_dev, inner,
+                                                 0.5 * tau))
+        elif kind == "tdpot":
+            x = dv.cached_vector(np.asarray(x_nodes, dtype=float), np.float64, dev)
+            for r in range(P):
+                self.ranks.append(SlabTdpotStepper(self.plan, r, locals_[r], list(mats), None, x))
         else:
             for r in range(P):
                 self.ranks.append(SlabStepper(self.plan, r, locals_[r], mats, comm=None))
 
-    def step(self):
+    def step(self, **kw):
         if self.exchange == "peer":
             for st in self.ranks:  # every rank stores its blocks into the others' receive buffers
                 st.pre_exchange()
@@ -325,12 +487,12 @@ class VirtualSlabGroup:
                 st.post_exchange()
             return
         P, bs = self.plan.P, self.plan.block
-        sends = [st.pre_exchange() for st in self.ranks]
+        sends = [st.begin_step(**kw) for st in self.ranks]
         for r, st in enumerate(self.ranks):
             for s in range(P):
                 st.recv[s * bs:(s + 1) * bs].copy_(sends[s][r * bs:(r + 1) * bs])
         for st in self.ranks:
-            st.post_exchange()
+            st.end_step(**kw)
 
     def gather(self):
         """The global state as a host numpy array (column-major)."""

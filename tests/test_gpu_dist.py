@@ -78,3 +78,52 @@ def test_virtual_ranks_match_single_gpu(P, n, steps, exchange):
         for _ in range(steps):
             o = orc.step(cache.exps, o)
         assert orc.rel_l2(got, o) <= 1e-12
+
+
+@pytest.mark.parametrize("P,n,steps", [(2, 64, 3), (4, 64, 2), (8, 64, 3), (8, 256, 2)])
+def test_virtual_ranks_gpe_strang(P, n, steps):
+    """Config 5 sharded: GPE Strang steps on P virtual slab ranks against the oracle's step
+    loop (problems.py:548-565, 597-598) and the single-GPU fused run."""
+    import torch
+
+    from paper_2103_01691_b200.problems import weighted_vortex_state
+
+    dev = torch.device("cuda", 0)
+    grids, lin_op, weights = km.gpe_setup(n)
+    psi = weighted_vortex_state(grids, weights)
+    tau = 0.1
+    cache = km.prepare(lin_op, tau)
+    grp = dist.VirtualSlabGroup(psi, cache, dev, P, kind="gpe", weights=weights, tau=tau)
+    for k in range(steps):
+        grp.step(k=k, steps=steps)
+    got = grp.gather()
+    want = psi
+    for _ in range(steps):
+        want = orc.gpe_strang_step(cache.exps, weights, want, tau)
+    assert orc.rel_l2(got, want) <= 1e-12
+    single = km.gpe_strang_run(cache, weights, psi, tau, steps)
+    assert orc.rel_l2(got, single) <= 1e-13
+
+
+@pytest.mark.parametrize("P,n,steps", [(2, 32, 3), (4, 64, 2), (8, 256, 3)])
+def test_virtual_ranks_tdpot_strang(P, n, steps):
+    """Config 4 sharded (256^3 over 8 ranks): E3 folded per step on every rank."""
+    import torch
+
+    from paper_2103_01691_b200.hermite import physical_propagator
+    from paper_2103_01691_b200.problems import schrodinger_initial_state
+
+    dev = torch.device("cuda", 0)
+    b = km.hermite_basis(n)
+    tau = 0.02
+    p = physical_propagator(b, tau)
+    cache = km.PropagatorCache(tau, (p, p, p))
+    psi = schrodinger_initial_state((b.nodes,) * 3)
+    grp = dist.VirtualSlabGroup(psi, cache, dev, P, kind="tdpot", x_nodes=b.nodes)
+    for s_ in range(steps):
+        grp.step(t=s_ * tau, tau=tau)
+    got = grp.gather()
+    want = psi
+    for s_ in range(steps):
+        want = orc.tdpot_strang_step(cache.exps, b.nodes, want, s_ * tau, tau)
+    assert orc.rel_l2(got, want) <= 1e-12

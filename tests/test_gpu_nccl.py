@@ -21,7 +21,8 @@ def _port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("n,steps,exchange", [(64, 3, "nccl"), (256, 2, "nccl"), (64, 3, "peer"), (256, 2, "peer")])
+@pytest.mark.parametrize("n,steps,exchange", [(64, 3, "nccl"), (256, 2, "nccl"), (64, 3, "peer"), (256, 2, "peer"),
+                                              (64, 3, "gpe"), (128, 2, "gpe"), (64, 3, "tdpot"), (128, 2, "tdpot")])
 def test_slab_stepper_over_nccl(n, steps, exchange):
     import torch
 

@@ -46,7 +46,7 @@ class CpuSlabStepper(dist.SlabStepper):
         self.recv = torch.zeros(self.a.size, dtype=torch.complex128)
         self.layout = "A"
 
-    def _run(self, calls, src, dst_final, scratch):
+    def _run(self, calls, src, dst_final, scratch, post=None):
         cur = src.numpy() if isinstance(src, torch.Tensor) else src
         for idx, (mu, m, nl, nmu, nr, kcb, kbs, ncb, nbs) in enumerate(calls):
             last = idx == len(calls) - 1
@@ -56,6 +56,8 @@ class CpuSlabStepper(dist.SlabStepper):
             y = orc.mu_mode_product(x, self.mats[mu], 2)
             scatter_out(dnp, y, ncb, nbs)
             cur = dnp
+        if post is not None:
+            self._phase(dst_final, post)
 
     def pre_exchange(self):
         before, _ = self.plan.even_calls() if self.layout == "A" else self.plan.odd_calls()
@@ -66,6 +68,49 @@ class CpuSlabStepper(dist.SlabStepper):
         _, after = self.plan.even_calls() if self.layout == "A" else self.plan.odd_calls()
         self._run(after, self.recv, self.a, self.w)
         self.layout = "B" if self.layout == "A" else "A"
+
+
+class CpuGpeStepper(CpuSlabStepper, dist.SlabGpeStepper):
+    """SlabGpeStepper's schedule with the phases as numpy (oracle nonlinear_half on the local
+    slab's weights, cut from the global vectors exactly as the device ops' pointer offsets)."""
+
+    def __init__(self, plan, rank, local_a, mats_np, comm, weights, half_tau):
+        CpuSlabStepper.__init__(self, plan, rank, local_a, mats_np, comm)
+        self.weights = [np.asarray(w, dtype=float) for w in weights]
+        self.half_tau = half_tau
+
+    def _op(self, layout, repeat):
+        return (layout, repeat)
+
+    def _phase(self, buf, op):
+        layout, repeat = op
+        n1, n2, n3 = self.plan.dims
+        c2, c3, r = self.plan.c2, self.plan.c3, self.rank
+        w1, w2, w3 = self.weights
+        if layout == "A":
+            shape, ws = (n1, n2, c3), (w1, w2, w3[r * c3:(r + 1) * c3])
+        else:
+            shape, ws = (n1, c2, n3), (w1, w2[r * c2:(r + 1) * c2], w3)
+        b = buf.numpy() if isinstance(buf, torch.Tensor) else buf
+        x = b.reshape(shape, order="F")
+        wp = orc.weight_product(ws, shape)
+        for _ in range(repeat):
+            x = orc.nonlinear_half(x, wp, self.half_tau)
+        b[:] = x.reshape(-1, order="F")
+
+
+class CpuTdpotStepper(CpuSlabStepper, dist.SlabTdpotStepper):
+    """SlabTdpotStepper's schedule with the per-step fold of E3 in numpy."""
+
+    def __init__(self, plan, rank, local_a, mats_np, comm, x_nodes):
+        CpuSlabStepper.__init__(self, plan, rank, local_a, list(mats_np), comm)
+        self.e3 = mats_np[2]
+        self.xn = np.asarray(x_nodes, dtype=float)
+
+    def begin_step(self, t=0.0, tau=0.0, **kw):
+        c_a, c_b = orc.sin2_integral(t, t + 0.5 * tau), orc.sin2_integral(t + 0.5 * tau, t + tau)
+        self.mats[2] = (np.exp(-1j * self.xn * c_b)[:, None] * self.e3) * np.exp(-1j * self.xn * c_a)[None, :]
+        return self.pre_exchange()
 
 
 def _free_port():
@@ -126,3 +171,60 @@ def test_slab_plan_blocks_partition_the_slab():
     plan = dist.SlabPlan((4, 8, 8), 4)
     assert plan.block * plan.P == plan.local
     assert plan.shape_a == (4, 8, 2) and plan.shape_b == (4, 2, 8)
+
+
+def _splitting_worker(rank, world, port, dims, steps, kind, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(7)
+        u = np.asfortranarray(rng.standard_normal(dims) + 1j * rng.standard_normal(dims)) * 0.7
+        mats = [rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)) for n in dims]
+        mats = [m / np.linalg.norm(m, 2) for m in mats]
+        plan = dist.SlabPlan(dims, world)
+        local = np.asfortranarray(plan.slab_a(u, rank)).reshape(-1, order="F")
+        tau = 0.1
+        if kind == "gpe":
+            ws = [rng.random(n) + 0.5 for n in dims]
+            st = CpuGpeStepper(plan, rank, local, mats, dist.NcclExchange(), ws, 0.5 * tau)
+            st.run(steps)
+            want = u
+            for _ in range(steps):
+                want = orc.gpe_strang_step(mats, ws, want, tau)
+        else:
+            x = np.linspace(-3.0, 3.0, dims[2])
+            st = CpuTdpotStepper(plan, rank, local, mats, dist.NcclExchange(), x)
+            st.run(0.25, tau, steps)
+            want = u
+            for s_ in range(steps):
+                want = orc.tdpot_strang_step(mats, x, want, 0.25 + s_ * tau, tau)
+        shape = plan.shape_a if st.layout == "A" else plan.shape_b
+        got = st.a.reshape(shape, order="F")
+        ref = plan.slab_a(want, rank) if st.layout == "A" else plan.slab_b(want, rank)
+        q.put((rank, st.layout, orc.rel_l2(got, ref)))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["gpe", "tdpot"])
+@pytest.mark.parametrize("steps", [1, 2, 3])
+def test_sharded_splitting_world2_matches_oracle(kind, steps):
+    """Configs 4 and 5 sharded: GPE Strang steps (phases on slab-offset weights, closing and
+    opening half-phases merged between steps) and TD-potential Strang steps (E3 folded per
+    step) over world-size 2 gloo, against the single-process oracle."""
+    world, dims = 2, (6, 16, 8)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_splitting_worker, args=(r, world, port, dims, steps, kind, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(world))
+    for rank, layout, err in res:
+        assert layout == ("B" if steps % 2 else "A")
+        assert err <= 1e-13, (rank, err)

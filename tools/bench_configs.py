@@ -164,14 +164,30 @@ def config4(budget, k=256):
     got = km.tdpot_strang_step(cache, b.nodes, psi, 0.3, tau)
     want = orc.tdpot_strang_step(cache.exps, b.nodes, psi, 0.3, tau)
     cpu_ms, kk = cpu_time(lambda: orc.tdpot_strang_step(cache.exps, b.nodes, psi, 0.3, tau), budget, 3)
-    # 8-rank slab decomposition run as 8 virtual ranks on this one GPU (schedule + fused pack/unpack kernels)
-    grp = dist.VirtualSlabGroup(psi, cache, DEV, 8)
-    ms_virtual8 = dev_time(grp.step, 5, warm=1)
+    # the 8-rank slab schedule of the TD-potential step (SlabTdpotStepper: per-step fold of E3 on
+    # every rank, fused pack/unpack, one exchange per step) run as 8 virtual ranks on this GPU;
+    # per-rank time = the group's time / 8 (every rank's kernels run back to back here)
+    grp = dist.VirtualSlabGroup(psi, cache, DEV, 8, kind="tdpot", x_nodes=b.nodes)
+    tt = [0.0]
+
+    def vstep():
+        grp.step(t=tt[0], tau=tau)
+        tt[0] += tau
+
+    ms_virtual8 = dev_time(vstep, 5, warm=1)
+    grp2 = dist.VirtualSlabGroup(psi, cache, DEV, 8, kind="tdpot", x_nodes=b.nodes)
+    for s_ in range(3):
+        grp2.step(t=0.3 + s_ * tau, tau=tau)
+    v8 = grp2.gather()
+    w8 = psi
+    for s_ in range(3):
+        w8 = orc.tdpot_strang_step(cache.exps, b.nodes, w8, 0.3 + s_ * tau, tau)
     flop = 8 * 3 * k**4
     return {"config": "4: TD-potential Strang 256^3 c128 (1 GPU; 8-rank schedule as virtual ranks)",
             "gpu_ms": ms, "tflops": flop / (ms * 1e-3) / 1e12, "cpu_ms": cpu_ms, "cpu_reps": kk,
             "speedup": cpu_ms / ms, "parity_rel_l2": orc.rel_l2(got, want),
-            "virtual8_linear_step_ms": ms_virtual8}
+            "virtual8_group_step_ms": ms_virtual8, "virtual8_per_rank_ms": ms_virtual8 / 8,
+            "virtual8_parity_rel_l2_3_steps": orc.rel_l2(v8, w8)}
 
 
 def config5(budget, n=512):
@@ -188,9 +204,29 @@ def config5(budget, n=512):
     p64 = dv.to_device(psi.astype(np.complex64), np.complex64, DEV)
     ms64 = dev_time(lambda: km.gpe_strang_step(c64, weights, p64, tau), 5)
     ms_run = dev_time(lambda: km.gpe_strang_run(cache, weights, p_dev, tau, 4), 2, warm=1) / 4
+    # the P-rank slab schedule (SlabGpeStepper) as P virtual ranks on this GPU: per-rank time
+    # = group time / P; parity of 2 steps against the single-GPU fused run
+    virtual = {}
+    for P in (2, 4, 8):
+        grp = dist.VirtualSlabGroup(psi, cache, DEV, P, kind="gpe", weights=weights, tau=tau)
+        kk_ = [0]
+
+        def vstep():
+            grp.step(k=kk_[0] % 2, steps=2)
+            kk_[0] += 1
+
+        gms = dev_time(vstep, 2, warm=2)
+        grp2 = dist.VirtualSlabGroup(psi, cache, DEV, P, kind="gpe", weights=weights, tau=tau)
+        for k_ in range(2):
+            grp2.step(k=k_, steps=2)
+        ref2 = km.gpe_strang_run(cache, weights, p_dev, tau, 2)
+        virtual[P] = {"group_step_ms": gms, "per_rank_ms": gms / P,
+                      "parity_vs_single_gpu_2_steps": orc.rel_l2(grp2.gather(), dv.to_host(ref2))}
+        del grp, grp2
     flop = 8 * 3 * n**4
     return {"config": "5: GPE 512^3 Strang step c128 (c64 input follows the reference's promotion to c128)",
             "gpu_ms": ms, "gpu_ms_c64_input": ms64, "gpu_ms_per_step_fused_run": ms_run,
+            "virtual_ranks": virtual,
             "tflops": flop / (ms * 1e-3) / 1e12, "cpu_ms": cpu_ms,
             "cpu_reps": kk, "speedup": cpu_ms / ms, "parity_rel_l2": orc.rel_l2(got, want)}
 

@@ -1,7 +1,11 @@
 """Run under torchrun (any world size): the NCCL slab stepper against a single-GPU
 reference computed on rank 0.  Exits non-zero on a parity failure.
 
-    torchrun --nproc-per-node P --master-addr 127.0.0.1 --master-port 29511 tools/slab_check.py [n] [steps] [nccl|peer]
+    torchrun --nproc-per-node P --master-addr 127.0.0.1 --master-port 29511 tools/slab_check.py [n] [steps] [nccl|peer|gpe|tdpot]
+
+nccl / peer: exact steps (SlabStepper / PeerSlabStepper) against LocalStepper;
+gpe: SlabGpeStepper.run (config 5) against gpe_strang_run on one GPU;
+tdpot: SlabTdpotStepper.run (config 4) against tdpot_strang_step on one GPU.
 """
 import os
 import sys
@@ -25,20 +29,44 @@ def main():
     torch.cuda.set_device(dev)
     tdist.init_process_group("nccl", device_id=dev)
     rank, world = tdist.get_rank(), tdist.get_world_size()
-    rng = np.random.default_rng(0)
-    u = np.asfortranarray(rng.standard_normal((n,) * 3) + 1j * rng.standard_normal((n,) * 3))
-    d2 = km.heat_factors(n, 2).factors[0]
-    cache = km.prepare(km.KroneckerOp((1j * d2,) * 3), 0.01)
-    cls = dist.PeerSlabStepper if exchange == "peer" else dist.SlabStepper
-    st = cls.from_global(u, cache, dev)
-    for _ in range(steps):
-        st.step()
+    if exchange == "gpe":
+        from paper_2103_01691_b200.problems import weighted_vortex_state
+
+        grids, lin_op, weights = km.gpe_setup(n)
+        u = weighted_vortex_state(grids, weights)
+        cache = km.prepare(lin_op, 0.1)
+        st = dist.SlabGpeStepper.from_global(u, cache, weights, 0.1, dev)
+        st.run(steps)
+        want = km.gpe_strang_run(cache, weights, u, 0.1, steps)
+    elif exchange == "tdpot":
+        from paper_2103_01691_b200.hermite import physical_propagator
+        from paper_2103_01691_b200.problems import schrodinger_initial_state
+
+        b = km.hermite_basis(n)
+        tau = 0.02
+        p = physical_propagator(b, tau)
+        cache = km.PropagatorCache(tau, (p, p, p))
+        u = schrodinger_initial_state((b.nodes,) * 3)
+        st = dist.SlabTdpotStepper.from_global(u, cache, b.nodes, dev)
+        st.run(0.0, tau, steps)
+        want = u
+        for s_ in range(steps):
+            want = km.tdpot_strang_step(cache, b.nodes, want, s_ * tau, tau)
+    else:
+        rng = np.random.default_rng(0)
+        u = np.asfortranarray(rng.standard_normal((n,) * 3) + 1j * rng.standard_normal((n,) * 3))
+        d2 = km.heat_factors(n, 2).factors[0]
+        cache = km.prepare(km.KroneckerOp((1j * d2,) * 3), 0.01)
+        cls = dist.PeerSlabStepper if exchange == "peer" else dist.SlabStepper
+        st = cls.from_global(u, cache, dev)
+        for _ in range(steps):
+            st.step()
+        ref = dist.LocalStepper(dv.to_device(u, np.complex128, dev), cache.device_exps((np.complex128,) * 3, dev))
+        for _ in range(steps):
+            ref.step()
+        want = dv.to_host(ref.state)
     torch.cuda.synchronize()
     mine = dv.to_host(st.local_state())
-    ref = dist.LocalStepper(dv.to_device(u, np.complex128, dev), cache.device_exps((np.complex128,) * 3, dev))
-    for _ in range(steps):
-        ref.step()
-    want = dv.to_host(ref.state)
     want_slab = st.plan.slab_a(want, rank) if st.layout == "A" else st.plan.slab_b(want, rank)
     err = float(np.linalg.norm((mine - want_slab).ravel()) / np.linalg.norm(want_slab.ravel()))
     errs = torch.tensor([err], device=dev)
