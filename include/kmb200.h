@@ -168,12 +168,14 @@ int km_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t 
  *     element (l, i, r) is at (i / out_block) * out_block_stride
  *                              + l + n_left*(i % out_block) + n_left*out_block*r.
  * in_block == n_mu / out_block == m are the plain layouts.  in_block must be a
- * multiple of 16 and out_block a multiple of 8 when they split.
+ * multiple of 16 and out_block a multiple of 8 when they split.  `post` (may be
+ * NULL) is fused into the epilogue as in km_mumode; it needs the plain output
+ * layout (out_block == m), the input may be blocked.
  */
 int km_mumode_split(const void* u, int u_dtype, const void* L, int L_dtype, void* out,
                     int64_t m, int64_t n_left, int64_t n_mu, int64_t n_right,
                     int32_t in_block, int64_t in_block_stride, int32_t out_block,
-                    int64_t out_block_stride, void* stream);
+                    int64_t out_block_stride, const km_pointop* post, void* stream);
 
 /*
  * μ-mode product whose output blocks are stored straight into other ranks'

@@ -173,8 +173,9 @@ int mumode_impl(const void* u, int udt, const void* L, int ldt, void* out, int64
       return fail(KM_EINVAL, "km_mumode_split: input block %d is not a multiple of %d", split->kcb, BK);
     if (nsplit && split->ncb % 8 != 0)
       return fail(KM_EINVAL, "km_mumode_split: output block %d is not a multiple of 8", split->ncb);
-    if ((ksplit || nsplit || fsplit) && op.kind != KM_OP_NONE)
-      return fail(KM_EINVAL, "km_mumode_split: pointwise ops are not supported on blocked layouts");
+    // a blocked INPUT only changes the loads; the fused op needs the plain output layout
+    if ((nsplit || fsplit) && op.kind != KM_OP_NONE)
+      return fail(KM_EINVAL, "km_mumode_split: pointwise ops are not supported on blocked output layouts");
     if (split->peer[0]) {
       const int64_t blocks = fsplit ? (M + split->fcb - 1) / split->fcb : (N + split->ncb - 1) / split->ncb;
       if (blocks > MAX_PEERS) return fail(KM_EINVAL, "km_mumode_peer: %lld output blocks exceed %d peers",
@@ -357,9 +358,9 @@ int km_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t 
 
 int km_mumode_split(const void* u, int u_dtype, const void* L, int L_dtype, void* out, int64_t m, int64_t n_left,
                     int64_t n_mu, int64_t n_right, int32_t in_block, int64_t in_block_stride, int32_t out_block,
-                    int64_t out_block_stride, void* stream) {
+                    int64_t out_block_stride, const km_pointop* post, void* stream) {
   Split sp{in_block, in_block_stride, out_block, out_block_stride};
-  return mumode_impl(u, u_dtype, L, L_dtype, out, m, n_left, n_mu, n_right, nullptr,
+  return mumode_impl(u, u_dtype, L, L_dtype, out, m, n_left, n_mu, n_right, post,
                      static_cast<cudaStream_t>(stream), &sp);
 }
 

@@ -75,6 +75,23 @@ class LocalStepper:
         return out
 
 
+class Prod:
+    """One product of a slab schedule: direction ``mu`` with matrix ``mat`` (a key of the
+    stepper's matrices: "E1", "E2", "E3", "E3p", "E3r0", "E3r1") of ``m`` rows, the
+    (n_left, n_mu, n_right) flattening, the blocked input / output (km_mumode_split) and the
+    source / destination buffers ("a", "w", "send", "recv") with element offsets."""
+
+    __slots__ = ("mu", "mat", "m", "nl", "nmu", "nr", "kcb", "kbs", "ncb", "nbs", "src", "soff", "dst", "doff")
+
+    def __init__(self, mu, mat, m, nl, nmu, nr, kcb, kbs, ncb, nbs, src, soff, dst, doff):
+        self.mu, self.mat, self.m, self.nl, self.nmu, self.nr = mu, mat, m, nl, nmu, nr
+        self.kcb, self.kbs, self.ncb, self.nbs = kcb, kbs, ncb, nbs
+        self.src, self.soff, self.dst, self.doff = src, soff, dst, doff
+
+    def plain_out(self):
+        return self.ncb == self.m
+
+
 class SlabPlan:
     """Index bookkeeping of the slab decomposition of a 3D state over P ranks.
 
@@ -116,6 +133,66 @@ class SlabPlan:
     def slab_b(self, u, rank):
         return u[:, rank * self.c2:(rank + 1) * self.c2, :]
 
+    def overlap_ok(self):
+        """The two-half schedule needs half-chunks of direction 3 that the blocked loaders take:
+        c3/2 a multiple of 16 (input blocks) and c2 a multiple of 16."""
+        return self.c3 % 32 == 0 and self.c2 % 16 == 0
+
+    def schedule(self, layout, overlap):
+        """One step from ``layout``: (pre, post, exchange), each pre/post a list of groups of
+        products :class:`Prod`; exchange ``h`` moves ``size`` elements at offset ``h * size`` of
+        the send / receive buffers after pre group ``h``; post group ``h`` reads only what
+        exchanges ``0..h`` delivered.
+
+        Serial (``overlap`` False): the schedule of :meth:`even_calls` / :meth:`odd_calls`, one
+        exchange of the whole slab.  Overlapped: the last product before the exchange runs in
+        two halves, each followed by its own all-to-all, so half 0 moves while half 1 computes:
+
+        * even (A -> B): direction 2 on the i3-halves of the slab (n_right = c3/2), per-peer
+          blocks of (n1, c2, c3/2); the receive buffer holds block (h, source q) at
+          ``(h*P + q) * bs/2``, which direction 3 reads as ONE blocked input (in_block = c3/2)
+          against E3 with its columns permuted to that order (``E3p``);
+        * odd (B -> A): direction 1, then direction 3 in two halves of output rows (``E3r0`` /
+          ``E3r1``: the rows of E3 whose i3 lie in the first / second half of every peer's
+          chunk), per-peer blocks of (n1, c2, c3/2); direction 2 then runs per half (i3 of
+          the half = its n_right) as soon as that half has arrived.
+        """
+        n1, n2, n3 = self.dims
+        c2, c3, bs, P = self.c2, self.c3, self.block, self.P
+        if not overlap:
+            if layout == "A":
+                pre = [[Prod(0, "E1", n1, 1, n1, n2 * c3, n1, 0, n1, 0, "a", 0, "w", 0),
+                        Prod(1, "E2", n2, n1, n2, c3, n2, 0, c2, bs, "w", 0, "send", 0)]]
+                post = [[Prod(2, "E3", n3, n1 * c2, n3, 1, n3, 0, n3, 0, "recv", 0, "a", 0)]]
+            else:
+                pre = [[Prod(2, "E3", n3, n1 * c2, n3, 1, n3, 0, n3, 0, "a", 0, "w", 0),
+                        Prod(0, "E1", n1, 1, n1, c2 * n3, n1, 0, n1, 0, "w", 0, "send", 0)]]
+                post = [[Prod(1, "E2", n2, n1, n2, c3, c2, bs, n2, 0, "recv", 0, "a", 0)]]
+            return pre, post, P * bs
+        h3, bsh = c3 // 2, bs // 2
+        if layout == "A":
+            pre = [[Prod(0, "E1", n1, 1, n1, n2 * c3, n1, 0, n1, 0, "a", 0, "w", 0),
+                    Prod(1, "E2", n2, n1, n2, h3, n2, 0, c2, bsh, "w", 0, "send", 0)],
+                   [Prod(1, "E2", n2, n1, n2, h3, n2, 0, c2, bsh, "w", n1 * n2 * h3, "send", P * bsh)]]
+            post = [[], [Prod(2, "E3p", n3, n1 * c2, n3, 1, h3, bsh, n3, 0, "recv", 0, "a", 0)]]
+        else:
+            pre = [[Prod(0, "E1", n1, 1, n1, c2 * n3, n1, 0, n1, 0, "a", 0, "w", 0),
+                    Prod(2, "E3r0", n3 // 2, n1 * c2, n3, 1, n3, 0, h3, bsh, "w", 0, "send", 0)],
+                   [Prod(2, "E3r1", n3 // 2, n1 * c2, n3, 1, n3, 0, h3, bsh, "w", 0, "send", P * bsh)]]
+            post = [[Prod(1, "E2", n2, n1, n2, h3, c2, bsh, n2, 0, "recv", 0, "a", 0)],
+                    [Prod(1, "E2", n2, n1, n2, h3, c2, bsh, n2, 0, "recv", P * bsh, "a", n1 * n2 * h3)]]
+        return pre, post, P * bsh
+
+    def e3_column_order(self):
+        """pi: column k' of E3p is column pi[k'] of E3 (the even-step receive order)."""
+        P, c3, h3 = self.P, self.c3, self.c3 // 2
+        return np.array([q * c3 + h * h3 + j for h in range(2) for q in range(P) for j in range(h3)])
+
+    def e3_row_halves(self):
+        """rho_g: row i' of E3r<g> is row rho_g[i'] of E3 (the odd-step send order)."""
+        P, c3, h3 = self.P, self.c3, self.c3 // 2
+        return [np.array([q * c3 + g * h3 + j for q in range(P) for j in range(h3)]) for g in range(2)]
+
     # product calls: (direction index, m, n_left, n_mu, n_right, in_block, in_stride, out_block, out_stride)
     def even_calls(self):
         """Layout A: directions 1, 2 (packed output) | exchange | direction 3 in layout B."""
@@ -148,7 +225,7 @@ class SlabStepper:
     B, after an even number in layout A (``self.layout``).
     """
 
-    def __init__(self, plan, rank, local_a, mats, comm):
+    def __init__(self, plan, rank, local_a, mats, comm, overlap=True):
         torch = dv.torch
         self.plan, self.rank, self.comm = plan, rank, comm
         self.mats = list(mats)
@@ -163,7 +240,28 @@ class SlabStepper:
         self.code = dv.code(dv.np_dtype(self.a.dtype))
         self.mcodes = [dv.code(dv.np_dtype(m.dtype)) for m in self.mats]
         self.lib = _native.lib()
-        self.launches_per_step = 3
+        self.overlap = bool(overlap) and plan.overlap_ok()
+        self.derived = {}
+        if self.overlap:
+            self._derive(self.mats[2])
+        self.launches_per_step = 4 if self.overlap else 3
+        self._works = []
+
+    def _derive(self, e3):
+        """E3 with permuted columns (even steps) and its two row halves (odd steps)."""
+        torch = dv.torch
+        pi = torch.as_tensor(self.plan.e3_column_order(), device=e3.device)
+        self.derived["E3p"] = e3.index_select(1, pi).contiguous()
+        for g, rho in enumerate(self.plan.e3_row_halves()):
+            self.derived[f"E3r{g}"] = e3.index_select(0, torch.as_tensor(rho, device=e3.device)).contiguous()
+
+    def _mat(self, key):
+        if key in ("E1", "E2", "E3"):
+            return self.mats[int(key[1]) - 1]
+        return self.derived[key]
+
+    def _buf(self, key):
+        return getattr(self, key) if isinstance(key, str) else key  # a name or the tensor itself
 
     @classmethod
     def from_global(cls, u_host, cache, dev, group=None):
@@ -175,27 +273,34 @@ class SlabStepper:
         mats = cache.device_exps((np.complex128,) * 3, dev)
         return cls(plan, rank, dv.as_fortran(local).permute(2, 1, 0).reshape(-1), mats, NcclExchange(group))
 
-    def _run(self, calls, src, dst_final, scratch, post=None):
-        """The products of one schedule half; ``post`` (a local-layout km_pointop of the layout
-        the last product writes) is fused into that product's epilogue when its layout is
-        plain and its direction is the last one, else applied as an in-place pass after it."""
+    def _exec(self, prods, post=None):
+        """Products through km_mumode_split; ``post`` (a km_pointop of the layout the last
+        product writes) is fused into its epilogue when that product writes the plain layout
+        along the last direction, else applied as an in-place pass over ``a`` afterwards."""
         stream = dv.stream_ptr(self.a.device)
-        cur = src
-        for idx, (mu, m, nl, nmu, nr, kcb, kbs, ncb, nbs) in enumerate(calls):
-            last = idx == len(calls) - 1
-            dst = dst_final if last else scratch
-            if last and post is not None and kcb == nmu and ncb == m and mu == len(self.plan.dims) - 1:
-                _native.check(self.lib.km_mumode(
-                    cur.data_ptr(), self.code, self.mats[mu].data_ptr(), self.mcodes[mu], dst.data_ptr(),
-                    m, nl, nmu, nr, ctypes.byref(post), stream))
+        es = self.a.element_size()
+        for idx, p in enumerate(prods):
+            fuse = (post is not None and idx == len(prods) - 1 and p.plain_out()
+                    and p.mu == len(self.plan.dims) - 1)
+            mat = self._mat(p.mat)
+            _native.check(self.lib.km_mumode_split(
+                self._buf(p.src).data_ptr() + es * p.soff, self.code, mat.data_ptr(), self.mcodes[p.mu],
+                self._buf(p.dst).data_ptr() + es * p.doff, p.m, p.nl, p.nmu, p.nr, p.kcb, p.kbs, p.ncb, p.nbs,
+                ctypes.byref(post) if fuse else None, stream))
+            if fuse:
                 post = None
-            else:
-                _native.check(self.lib.km_mumode_split(
-                    cur.data_ptr(), self.code, self.mats[mu].data_ptr(), self.mcodes[mu], dst.data_ptr(),
-                    m, nl, nmu, nr, kcb, kbs, ncb, nbs, stream))
-            cur = dst
         if post is not None:
-            self._phase(dst_final, post)
+            self._phase(self.a, post)
+
+    def _run(self, calls, src, dst_final, scratch, post=None):
+        """Serial products from (mu, m, nl, nmu, nr, kcb, kbs, ncb, nbs) tuples on explicit
+        tensors (PeerSlabStepper's schedule)."""
+        prods, cur = [], src
+        for idx, (mu, m, nl, nmu, nr, kcb, kbs, ncb, nbs) in enumerate(calls):
+            dst = dst_final if idx == len(calls) - 1 else scratch
+            prods.append(Prod(mu, f"E{mu + 1}", m, nl, nmu, nr, kcb, kbs, ncb, nbs, cur, 0, dst, 0))
+            cur = dst
+        self._exec(prods, post)
 
     def _phase(self, buf, op):
         """In-place standalone pointwise pass over the local slab."""
@@ -213,17 +318,40 @@ class SlabStepper:
         self.layout = "B" if self.layout == "A" else "A"
 
     def begin_step(self, **kw):
-        """Everything of one step before its exchange; returns the send buffer."""
-        return self.pre_exchange()
+        """Everything of one step before and including the launch of its exchange(s): the
+        products of each pre group, each followed by its all-to-all (asynchronous on the
+        communicator's stream when ``comm`` is set; a virtual group moves the blocks itself).
+        Returns the send buffer."""
+        pre, _, size = self.plan.schedule(self.layout, self.overlap)
+        self._works = []
+        for h, group in enumerate(pre):
+            self._exec(group)
+            if self.comm is not None:
+                self._works.append(self.comm.exchange_async(self.recv[h * size:(h + 1) * size],
+                                                            self.send[h * size:(h + 1) * size]))
+        return self.send
 
-    def end_step(self, **kw):
-        """Everything of one step after its exchange."""
-        self.post_exchange()
+    def end_step(self, post=None, **kw):
+        """The products after the exchange; post group h waits only for exchange h.  ``post``
+        is a pointwise op on the layout the step ends in (fused where the kernel can)."""
+        _, groups, _ = self.plan.schedule(self.layout, self.overlap)
+        live = [i for i, g in enumerate(groups) if g]
+        for h, group in enumerate(groups):
+            if h < len(self._works):
+                self._works[h].wait()
+            if group:
+                self._exec(group, post if h == live[-1] else None)
+        self._works = []
+        self.layout = "B" if self.layout == "A" else "A"
 
     def step(self, **kw):
         self.begin_step(**kw)
-        self.comm.exchange(self.recv, self.send)
         self.end_step(**kw)
+
+    def exchange_halves(self):
+        """(number of exchanges, elements each) of a step from the current layout."""
+        pre, _, size = self.plan.schedule(self.layout, self.overlap)
+        return len(pre), size
 
     def local_state(self):
         """The local slab as a column-major (n1, n2, c3) [layout A] or (n1, c2, n3) [layout B] tensor view."""
@@ -252,12 +380,12 @@ class SlabGpeStepper(SlabStepper):
     applies the single opening and closing phases at the ends.
     """
 
-    def __init__(self, plan, rank, local_a, mats, comm, weights_dev, inner_dev, half_tau):
-        super().__init__(plan, rank, local_a, mats, comm)
+    def __init__(self, plan, rank, local_a, mats, comm, weights_dev, inner_dev, half_tau, overlap=True):
+        super().__init__(plan, rank, local_a, mats, comm, overlap=overlap)
         self.wdev = list(weights_dev)
         self.inner = inner_dev
         self.coef = 0.5 * half_tau  # problems.py:545
-        self.launches_per_step = 4
+        self.launches_per_step += 1
 
     def _op(self, layout, repeat):
         n1, n2, n3 = self.plan.dims
@@ -281,13 +409,11 @@ class SlabGpeStepper(SlabStepper):
     def begin_step(self, k=0, steps=1, **kw):
         if k == 0:
             self._phase(self.a, self._op(self.layout, 1))
-        return self.pre_exchange()
+        return super().begin_step()
 
     def end_step(self, k=0, steps=1, **kw):
-        _, after = self.plan.even_calls() if self.layout == "A" else self.plan.odd_calls()
         out_layout = "B" if self.layout == "A" else "A"
-        self._run(after, self.recv, self.a, self.w, post=self._op(out_layout, 1 if k == steps - 1 else 2))
-        self.layout = out_layout
+        super().end_step(post=self._op(out_layout, 1 if k == steps - 1 else 2))
 
     def run(self, steps):
         for k in range(steps):
@@ -320,23 +446,40 @@ class SlabTdpotStepper(SlabStepper):
     plain slab step, one exchange per step.  ``begin_step(t=, tau=)``.
     """
 
-    def __init__(self, plan, rank, local_a, mats, comm, x_nodes_dev):
-        super().__init__(plan, rank, local_a, mats, comm)
+    def __init__(self, plan, rank, local_a, mats, comm, x_nodes_dev, overlap=True):
+        super().__init__(plan, rank, local_a, mats, comm, overlap=overlap)
+        torch = dv.torch
         self.e3 = self.mats[2]
-        self.folded = dv.torch.empty_like(self.e3)
+        self.folded = torch.empty_like(self.e3)
         self.x = x_nodes_dev
-        self.launches_per_step = 4
+        # the derived forms of E3 (permuted columns, row halves) are folded per step from their
+        # own unfolded copies, with the node vector permuted the same way
+        self.base = {k: v.clone() for k, v in self.derived.items()}
+        self.x_perm = None
+        if self.overlap:
+            self.x_perm = self.x.index_select(0, torch.as_tensor(plan.e3_column_order(), device=self.x.device))
+            self.x_rows = [self.x.index_select(0, torch.as_tensor(r, device=self.x.device))
+                           for r in plan.e3_row_halves()]
+        self.launches_per_step += 1
+
+    def _fold(self, src, dst, x_rows, x_cols, c_a, c_b):
+        m, k = src.shape
+        _native.check(self.lib.km_diag_phase_fold(src.data_ptr(), dst.data_ptr(), m, k, x_rows.data_ptr(),
+                                                  x_cols.data_ptr(), c_a, c_b, dv.stream_ptr(self.a.device)))
 
     def begin_step(self, t=0.0, tau=0.0, **kw):
         from .problems import sin2_integral
 
         c_a, c_b = sin2_integral(t, t + 0.5 * tau), sin2_integral(t + 0.5 * tau, t + tau)
-        m, k = self.e3.shape
-        _native.check(self.lib.km_diag_phase_fold(self.e3.data_ptr(), self.folded.data_ptr(), m, k,
-                                                  self.x.data_ptr(), self.x.data_ptr(), c_a, c_b,
-                                                  dv.stream_ptr(self.a.device)))
-        self.mats[2] = self.folded
-        return self.pre_exchange()
+        if not self.overlap:
+            self._fold(self.e3, self.folded, self.x, self.x, c_a, c_b)
+            self.mats[2] = self.folded
+        elif self.layout == "A":  # even step: E3 with permuted columns
+            self._fold(self.base["E3p"], self.derived["E3p"], self.x, self.x_perm, c_a, c_b)
+        else:  # odd step: the two row halves
+            for g in range(2):
+                self._fold(self.base[f"E3r{g}"], self.derived[f"E3r{g}"], self.x_rows[g], self.x, c_a, c_b)
+        return super().begin_step()
 
     def run(self, t0, tau, steps):
         for s_ in range(steps):
@@ -369,7 +512,7 @@ class PeerSlabStepper(SlabStepper):
     """
 
     def __init__(self, plan, rank, local_a, mats, recv_pair, peer_ptrs, barrier):
-        super().__init__(plan, rank, local_a, mats, comm=None)
+        super().__init__(plan, rank, local_a, mats, comm=None, overlap=False)
         self.send = None
         self.recv_pair = recv_pair
         self.peer_ptrs = [(ctypes.c_void_p * plan.P)(*ptrs) for ptrs in peer_ptrs]
@@ -430,10 +573,15 @@ class NcclExchange:
         self.group = group
 
     def exchange(self, recv, send):
+        self.exchange_async(recv, send).wait()
+
+    def exchange_async(self, recv, send):
+        """Start the all-to-all; it runs on NCCL's stream after the work already queued on the
+        current stream, and ``.wait()`` on the returned handle makes the current stream wait."""
         t = dv.torch
         r = t.view_as_real(recv) if recv.is_complex() else recv
         s = t.view_as_real(send) if send.is_complex() else send
-        self.tdist.all_to_all_single(r.reshape(-1), s.reshape(-1), group=self.group)
+        return self.tdist.all_to_all_single(r.reshape(-1), s.reshape(-1), group=self.group, async_op=True)
 
 
 class VirtualSlabGroup:
@@ -445,7 +593,7 @@ class VirtualSlabGroup:
     """
 
     def __init__(self, u_host, cache, dev, P, exchange="nccl", kind="plain", weights=None, tau=None,
-                 x_nodes=None):
+                 x_nodes=None, overlap=True):
         """``kind``: "plain" (exact steps), "gpe" (SlabGpeStepper: ``weights``, ``tau``) or
         "tdpot" (SlabTdpotStepper: ``x_nodes``)."""
         self.plan = SlabPlan(u_host.shape, P)
@@ -470,14 +618,14 @@ class VirtualSlabGroup:
             inner = dv.cached_vector(inner_weight_product(weights, u_host.shape), np.float64, dev)
             for r in range(P):
                 self.ranks.append(SlabGpeStepper(self.plan, r, locals_[r], list(mats), None, w_dev, inner,
-                                                 0.5 * tau))
+                                                 0.5 * tau, overlap=overlap))
         elif kind == "tdpot":
             x = dv.cached_vector(np.asarray(x_nodes, dtype=float), np.float64, dev)
             for r in range(P):
-                self.ranks.append(SlabTdpotStepper(self.plan, r, locals_[r], list(mats), None, x))
+                self.ranks.append(SlabTdpotStepper(self.plan, r, locals_[r], list(mats), None, x, overlap=overlap))
         else:
             for r in range(P):
-                self.ranks.append(SlabStepper(self.plan, r, locals_[r], mats, comm=None))
+                self.ranks.append(SlabStepper(self.plan, r, locals_[r], mats, comm=None, overlap=overlap))
 
     def step(self, **kw):
         if self.exchange == "peer":
@@ -486,11 +634,15 @@ class VirtualSlabGroup:
             for st in self.ranks:
                 st.post_exchange()
             return
-        P, bs = self.plan.P, self.plan.block
+        P = self.plan.P
+        halves, size = self.ranks[0].exchange_halves()
+        blk = size // P
         sends = [st.begin_step(**kw) for st in self.ranks]
-        for r, st in enumerate(self.ranks):
-            for s in range(P):
-                st.recv[s * bs:(s + 1) * bs].copy_(sends[s][r * bs:(r + 1) * bs])
+        for h in range(halves):  # the all-to-all of each half: recv_r[h][s] = send_s[h][r]
+            base = h * size
+            for r, st in enumerate(self.ranks):
+                for s in range(P):
+                    st.recv[base + s * blk:base + (s + 1) * blk].copy_(sends[s][base + r * blk:base + (r + 1) * blk])
         for st in self.ranks:
             st.end_step(**kw)
 

@@ -39,7 +39,7 @@ def test_split_kernel_addressing():
     L_d = torch.from_numpy(np.ascontiguousarray(L)).to(dev)
     _native.check(_native.lib().km_mumode_split(
         src_d.data_ptr(), _native.KM_C128, L_d.data_ptr(), _native.KM_C128, out_d.data_ptr(),
-        m, nl, nmu, nr, kcb, kbs, ncb, nbs, dv.stream_ptr(dev)))
+        m, nl, nmu, nr, kcb, kbs, ncb, nbs, None, dv.stream_ptr(dev)))
     out = out_d.cpu().numpy()
     got = np.concatenate([out[b * nbs: b * nbs + nl * ncb * nr].reshape((nl, ncb, nr), order="F")
                           for b in range(m // ncb)], axis=1)
@@ -49,14 +49,15 @@ def test_split_kernel_addressing():
 def test_split_rejects_bad_blocks():
     lib = _native.lib()
     p = ctypes.c_void_p(16)
-    assert lib.km_mumode_split(p, 3, p, 3, p, 16, 4, 20, 2, 10, 40, 16, 0, None) == _native.KM_EINVAL
-    assert lib.km_mumode_split(p, 3, p, 3, p, 16, 1, 32, 2, 16, 64, 16, 0, None) == _native.KM_EINVAL
+    assert lib.km_mumode_split(p, 3, p, 3, p, 16, 4, 20, 2, 10, 40, 16, 0, None, None) == _native.KM_EINVAL
+    assert lib.km_mumode_split(p, 3, p, 3, p, 16, 1, 32, 2, 16, 64, 16, 0, None, None) == _native.KM_EINVAL
 
 
-@pytest.mark.parametrize("P,n,steps,exchange", [(2, 64, 3, "nccl"), (4, 64, 4, "nccl"), (8, 256, 3, "nccl"),
-                                                (2, 64, 3, "peer"), (4, 64, 4, "peer"), (8, 256, 3, "peer"),
-                                                (2, 256, 2, "peer")])
-def test_virtual_ranks_match_single_gpu(P, n, steps, exchange):
+@pytest.mark.parametrize("P,n,steps,exchange,overlap", [
+    (2, 64, 3, "nccl", True), (4, 64, 4, "nccl", True), (8, 256, 3, "nccl", True), (8, 256, 2, "nccl", False),
+    (4, 256, 2, "nccl", True), (2, 64, 3, "peer", False), (4, 64, 4, "peer", False), (8, 256, 3, "peer", False),
+    (2, 256, 2, "peer", False)])
+def test_virtual_ranks_match_single_gpu(P, n, steps, exchange, overlap):
     import torch
 
     dev = torch.device("cuda", 0)
@@ -64,7 +65,9 @@ def test_virtual_ranks_match_single_gpu(P, n, steps, exchange):
     u = crand(rng, (n,) * 3)
     d2 = km.heat_factors(n, 2).factors[0]
     cache = km.prepare(km.KroneckerOp((1j * d2,) * 3), 0.01)
-    grp = dist.VirtualSlabGroup(u, cache, dev, P, exchange=exchange)
+    grp = dist.VirtualSlabGroup(u, cache, dev, P, exchange=exchange, overlap=overlap)
+    if exchange == "nccl":
+        assert grp.ranks[0].overlap == (overlap and grp.plan.overlap_ok())
     for _ in range(steps):
         grp.step()
     got = grp.gather()
@@ -80,8 +83,9 @@ def test_virtual_ranks_match_single_gpu(P, n, steps, exchange):
         assert orc.rel_l2(got, o) <= 1e-12
 
 
-@pytest.mark.parametrize("P,n,steps", [(2, 64, 3), (4, 64, 2), (8, 64, 3), (8, 256, 2)])
-def test_virtual_ranks_gpe_strang(P, n, steps):
+@pytest.mark.parametrize("P,n,steps,overlap", [(2, 64, 3, True), (4, 64, 2, True), (8, 128, 3, True),
+                                               (8, 256, 2, True), (8, 256, 3, False)])
+def test_virtual_ranks_gpe_strang(P, n, steps, overlap):
     """Config 5 sharded: GPE Strang steps on P virtual slab ranks against the oracle's step
     loop (problems.py:548-565, 597-598) and the single-GPU fused run."""
     import torch
@@ -93,7 +97,7 @@ def test_virtual_ranks_gpe_strang(P, n, steps):
     psi = weighted_vortex_state(grids, weights)
     tau = 0.1
     cache = km.prepare(lin_op, tau)
-    grp = dist.VirtualSlabGroup(psi, cache, dev, P, kind="gpe", weights=weights, tau=tau)
+    grp = dist.VirtualSlabGroup(psi, cache, dev, P, kind="gpe", weights=weights, tau=tau, overlap=overlap)
     for k in range(steps):
         grp.step(k=k, steps=steps)
     got = grp.gather()
@@ -105,8 +109,9 @@ def test_virtual_ranks_gpe_strang(P, n, steps):
     assert orc.rel_l2(got, single) <= 1e-13
 
 
-@pytest.mark.parametrize("P,n,steps", [(2, 32, 3), (4, 64, 2), (8, 256, 3)])
-def test_virtual_ranks_tdpot_strang(P, n, steps):
+@pytest.mark.parametrize("P,n,steps,overlap", [(2, 32, 3, True), (2, 64, 3, True), (4, 64, 2, True),
+                                               (8, 256, 3, True), (8, 256, 2, False)])
+def test_virtual_ranks_tdpot_strang(P, n, steps, overlap):
     """Config 4 sharded (256^3 over 8 ranks): E3 folded per step on every rank."""
     import torch
 
@@ -119,7 +124,7 @@ def test_virtual_ranks_tdpot_strang(P, n, steps):
     p = physical_propagator(b, tau)
     cache = km.PropagatorCache(tau, (p, p, p))
     psi = schrodinger_initial_state((b.nodes,) * 3)
-    grp = dist.VirtualSlabGroup(psi, cache, dev, P, kind="tdpot", x_nodes=b.nodes)
+    grp = dist.VirtualSlabGroup(psi, cache, dev, P, kind="tdpot", x_nodes=b.nodes, overlap=overlap)
     for s_ in range(steps):
         grp.step(t=s_ * tau, tau=tau)
     got = grp.gather()

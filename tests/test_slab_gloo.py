@@ -35,47 +35,50 @@ def scatter_out(buf, x, ncb, nbs):
 
 
 class CpuSlabStepper(dist.SlabStepper):
-    """SlabStepper whose products run on the CPU oracle (test double for the kernels)."""
+    """SlabStepper whose products run on the CPU oracle (test double for the kernels): the
+    schedule (serial or two-half overlapped), the blocked addressing and the derived forms of
+    E3 are the stepper's own; only the product itself is the oracle's."""
 
-    def __init__(self, plan, rank, local_a, mats_np, comm):
+    def __init__(self, plan, rank, local_a, mats_np, comm, overlap=True):
         self.plan, self.rank, self.comm = plan, rank, comm
-        self.mats = mats_np
+        self.mats = list(mats_np)
         self.a = local_a.copy()
         self.w = np.empty_like(self.a)
         self.send = torch.zeros(self.a.size, dtype=torch.complex128)
         self.recv = torch.zeros(self.a.size, dtype=torch.complex128)
         self.layout = "A"
+        self.overlap = overlap and plan.overlap_ok()
+        self.derived = {}
+        if self.overlap:
+            self._derive(self.mats[2])
+        self._works = []
 
-    def _run(self, calls, src, dst_final, scratch, post=None):
-        cur = src.numpy() if isinstance(src, torch.Tensor) else src
-        for idx, (mu, m, nl, nmu, nr, kcb, kbs, ncb, nbs) in enumerate(calls):
-            last = idx == len(calls) - 1
-            dst = dst_final if last else scratch
-            dnp = dst.numpy() if isinstance(dst, torch.Tensor) else dst
-            x = gather_in(cur, nl, nmu, nr, kcb, kbs)
-            y = orc.mu_mode_product(x, self.mats[mu], 2)
-            scatter_out(dnp, y, ncb, nbs)
-            cur = dnp
+    def _derive(self, e3):
+        self.derived["E3p"] = e3[:, self.plan.e3_column_order()]
+        for g, rho in enumerate(self.plan.e3_row_halves()):
+            self.derived[f"E3r{g}"] = e3[rho, :]
+
+    def _np(self, key):
+        b = self._buf(key)
+        return b.numpy() if isinstance(b, torch.Tensor) else b
+
+    def _exec(self, prods, post=None):
+        for p in prods:
+            src = self._np(p.src)[p.soff:]
+            dst = self._np(p.dst)[p.doff:]
+            x = gather_in(src, p.nl, p.nmu, p.nr, p.kcb, p.kbs)
+            y = orc.mu_mode_product(x, self._mat(p.mat), 2)
+            scatter_out(dst, y, p.ncb, p.nbs)
         if post is not None:
-            self._phase(dst_final, post)
-
-    def pre_exchange(self):
-        before, _ = self.plan.even_calls() if self.layout == "A" else self.plan.odd_calls()
-        self._run(before, self.a, self.send, self.w)
-        return self.send
-
-    def post_exchange(self):
-        _, after = self.plan.even_calls() if self.layout == "A" else self.plan.odd_calls()
-        self._run(after, self.recv, self.a, self.w)
-        self.layout = "B" if self.layout == "A" else "A"
+            self._phase(self.a, post)
 
 
 class CpuGpeStepper(CpuSlabStepper, dist.SlabGpeStepper):
     """SlabGpeStepper's schedule with the phases as numpy (oracle nonlinear_half on the local
     slab's weights, cut from the global vectors exactly as the device ops' pointer offsets)."""
 
-    def __init__(self, plan, rank, local_a, mats_np, comm, weights, half_tau):
-        CpuSlabStepper.__init__(self, plan, rank, local_a, mats_np, comm)
+    def __init__(self, plan, rank, local_a, mats_np, comm, weights, half_tau, overlap=True):
+        CpuSlabStepper.__init__(self, plan, rank, local_a, mats_np, comm, overlap)
         self.weights = [np.asarray(w, dtype=float) for w in weights]
         self.half_tau = half_tau
 
@@ -102,15 +105,17 @@ class CpuGpeStepper(CpuSlabStepper, dist.SlabGpeStepper):
 class CpuTdpotStepper(CpuSlabStepper, dist.SlabTdpotStepper):
     """SlabTdpotStepper's schedule with the per-step fold of E3 in numpy."""
 
-    def __init__(self, plan, rank, local_a, mats_np, comm, x_nodes):
-        CpuSlabStepper.__init__(self, plan, rank, local_a, list(mats_np), comm)
+    def __init__(self, plan, rank, local_a, mats_np, comm, x_nodes, overlap=True):
+        CpuSlabStepper.__init__(self, plan, rank, local_a, list(mats_np), comm, overlap)
         self.e3 = mats_np[2]
         self.xn = np.asarray(x_nodes, dtype=float)
 
     def begin_step(self, t=0.0, tau=0.0, **kw):
         c_a, c_b = orc.sin2_integral(t, t + 0.5 * tau), orc.sin2_integral(t + 0.5 * tau, t + tau)
         self.mats[2] = (np.exp(-1j * self.xn * c_b)[:, None] * self.e3) * np.exp(-1j * self.xn * c_a)[None, :]
-        return self.pre_exchange()
+        if self.overlap:
+            self._derive(self.mats[2])
+        return dist.SlabStepper.begin_step(self)
 
 
 def _free_port():
@@ -119,7 +124,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, dims, steps, q):
+def _worker(rank, world, port, dims, steps, q, overlap=True):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     tdist.init_process_group("gloo", rank=rank, world_size=world)
@@ -130,7 +135,7 @@ def _worker(rank, world, port, dims, steps, q):
         mats = [m / np.linalg.norm(m, 2) for m in mats]
         plan = dist.SlabPlan(dims, world)
         local = np.asfortranarray(plan.slab_a(u, rank)).reshape(-1, order="F")
-        st = CpuSlabStepper(plan, rank, local, mats, dist.NcclExchange())
+        st = CpuSlabStepper(plan, rank, local, mats, dist.NcclExchange(), overlap)
         for _ in range(steps):
             st.step()
         want = u
@@ -144,13 +149,17 @@ def _worker(rank, world, port, dims, steps, q):
         tdist.destroy_process_group()
 
 
+@pytest.mark.parametrize("overlap", [False, True])
 @pytest.mark.parametrize("steps", [1, 2, 3])
-def test_slab_schedule_world2_matches_oracle(steps):
-    world, dims = 2, (6, 32, 8)
+def test_slab_schedule_world2_matches_oracle(steps, overlap):
+    """Serial schedule and the two-half overlapped one (asynchronous all-to-all per half,
+    permuted E3 columns on even steps, E3 row halves on odd steps)."""
+    world, dims = 2, (6, 32, 64)
+    assert dist.SlabPlan(dims, world).overlap_ok()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, steps, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, steps, q, overlap)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
@@ -173,7 +182,7 @@ def test_slab_plan_blocks_partition_the_slab():
     assert plan.shape_a == (4, 8, 2) and plan.shape_b == (4, 2, 8)
 
 
-def _splitting_worker(rank, world, port, dims, steps, kind, q):
+def _splitting_worker(rank, world, port, dims, steps, kind, q, overlap=True):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     tdist.init_process_group("gloo", rank=rank, world_size=world)
@@ -187,14 +196,14 @@ def _splitting_worker(rank, world, port, dims, steps, kind, q):
         tau = 0.1
         if kind == "gpe":
             ws = [rng.random(n) + 0.5 for n in dims]
-            st = CpuGpeStepper(plan, rank, local, mats, dist.NcclExchange(), ws, 0.5 * tau)
+            st = CpuGpeStepper(plan, rank, local, mats, dist.NcclExchange(), ws, 0.5 * tau, overlap)
             st.run(steps)
             want = u
             for _ in range(steps):
                 want = orc.gpe_strang_step(mats, ws, want, tau)
         else:
             x = np.linspace(-3.0, 3.0, dims[2])
-            st = CpuTdpotStepper(plan, rank, local, mats, dist.NcclExchange(), x)
+            st = CpuTdpotStepper(plan, rank, local, mats, dist.NcclExchange(), x, overlap)
             st.run(0.25, tau, steps)
             want = u
             for s_ in range(steps):
@@ -207,17 +216,18 @@ def _splitting_worker(rank, world, port, dims, steps, kind, q):
         tdist.destroy_process_group()
 
 
+@pytest.mark.parametrize("overlap", [False, True])
 @pytest.mark.parametrize("kind", ["gpe", "tdpot"])
-@pytest.mark.parametrize("steps", [1, 2, 3])
-def test_sharded_splitting_world2_matches_oracle(kind, steps):
+@pytest.mark.parametrize("steps", [1, 2])
+def test_sharded_splitting_world2_matches_oracle(kind, steps, overlap):
     """Configs 4 and 5 sharded: GPE Strang steps (phases on slab-offset weights, closing and
     opening half-phases merged between steps) and TD-potential Strang steps (E3 folded per
     step) over world-size 2 gloo, against the single-process oracle."""
-    world, dims = 2, (6, 16, 8)
+    world, dims = 2, (6, 32, 64)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_splitting_worker, args=(r, world, port, dims, steps, kind, q))
+    procs = [ctx.Process(target=_splitting_worker, args=(r, world, port, dims, steps, kind, q, overlap))
              for r in range(world)]
     for p in procs:
         p.start()
