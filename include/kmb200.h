@@ -171,11 +171,16 @@ int km_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t 
  * multiple of 16 and out_block a multiple of 8 when they split.  `post` (may be
  * NULL) is fused into the epilogue as in km_mumode; it needs the plain output
  * layout (out_block == m), the input may be blocked.
+ * accumulate = 1 adds the product into `out` instead of overwriting it,
+ * out = post(out + u ×_μ L), each element rounded as numpy's `out += p`
+ * (kron.py:99-101, the Kronecker-sum matvec; and the K-split halves of the
+ * slab step).  The DMMA kernels only (complex64 x complex64 included).
  */
 int km_mumode_split(const void* u, int u_dtype, const void* L, int L_dtype, void* out,
                     int64_t m, int64_t n_left, int64_t n_mu, int64_t n_right,
                     int32_t in_block, int64_t in_block_stride, int32_t out_block,
-                    int64_t out_block_stride, const km_pointop* post, void* stream);
+                    int64_t out_block_stride, int32_t accumulate, const km_pointop* post,
+                    void* stream);
 
 /*
  * μ-mode product whose output blocks are stored straight into other ranks'

@@ -82,7 +82,7 @@ def _declare(lib):
     lib.km_mumode.argtypes = [c_vp, c_int, c_vp, c_int, c_vp, c_i64, c_i64, c_i64, c_i64, p_op, c_vp]
     lib.km_mumode_split.restype = c_int
     lib.km_mumode_split.argtypes = [c_vp, c_int, c_vp, c_int, c_vp, c_i64, c_i64, c_i64, c_i64,
-                                    ctypes.c_int32, c_i64, ctypes.c_int32, c_i64, p_op, c_vp]
+                                    ctypes.c_int32, c_i64, ctypes.c_int32, c_i64, ctypes.c_int32, p_op, c_vp]
     lib.km_mumode_fibers.restype = c_int
     lib.km_mumode_fibers.argtypes = [c_vp, c_int, c_vp, c_int, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp]
     lib.km_diag_phase_fold.restype = c_int

@@ -167,6 +167,8 @@ int mumode_impl(const void* u, int udt, const void* L, int ldt, void* out, int64
                   split->ncb, K, N);
     if ((ksplit || nsplit) && nl == 1)
       return fail(KM_EINVAL, "km_mumode_split: blocked layouts need n_left > 1");
+    if (split->acc && split->peer[0])
+      return fail(KM_EINVAL, "km_mumode_peer: no accumulation into peer outputs");
     if (fsplit && (nl != 1 || nsplit || !split->peer[0]))
       return fail(KM_EINVAL, "km_mumode_peer: fiber blocks need n_left == 1, unsplit rows and peer outputs");
     if (ksplit && split->kcb % BK != 0)
@@ -358,8 +360,11 @@ int km_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t 
 
 int km_mumode_split(const void* u, int u_dtype, const void* L, int L_dtype, void* out, int64_t m, int64_t n_left,
                     int64_t n_mu, int64_t n_right, int32_t in_block, int64_t in_block_stride, int32_t out_block,
-                    int64_t out_block_stride, const km_pointop* post, void* stream) {
+                    int64_t out_block_stride, int32_t accumulate, const km_pointop* post, void* stream) {
+  if (accumulate != 0 && accumulate != 1)
+    return fail(KM_EINVAL, "km_mumode_split: accumulate must be 0 or 1, got %d", accumulate);
   Split sp{in_block, in_block_stride, out_block, out_block_stride};
+  sp.acc = accumulate;
   return mumode_impl(u, u_dtype, L, L_dtype, out, m, n_left, n_mu, n_right, post,
                      static_cast<cudaStream_t>(stream), &sp);
 }

@@ -390,13 +390,12 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
     const bool plain_rows = sp.ncb >= N && !sp.peer[0];
     const int64_t f_q = KC ? 0 : m0 / nl;
     const int64_t f_rem = KC ? 0 : m0 - f_q * nl, f_slab = KC ? 0 : f_q * nl * sp.ncb;
-    // one 8-row block of the warp tile: row i (runtime) with accumulators crow/cirow
-    // (with_op false: the values were already transformed, gpe_rows below)
-    auto emit_row = [&](const int i, const double (&crow)[4][2], const double (&cirow)[4][2], const bool with_op) {
+    using TO = typename El<double, CU || CL>::T;
+    // visit the output addresses of one 8-row block of the warp tile: fn(dst, p, j, h, col)
+    // for every in-range element of row i
+    auto visit_row = [&](const int i, auto&& fn) {
       const int64_t f = m0 + wm + i * 8 + g;
       if (f >= M) return;
-      const double lf = with_op ? split_fiber_weight<OPK>(op, f) : 0.0;
-      using TO = typename El<double, CU || CL>::T;
       const int64_t cs = KC ? 1 : nl;
       TO* obase = out;
       int64_t ob;
@@ -423,16 +422,40 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
         for (int h = 0; h < 2; ++h) {
           const int col = c8 + 2 * t + h;
           if (col >= N) continue;
-          const int64_t p = obj + static_cast<int64_t>(col) * cs;
-          double re = crow[j][h], im = (CU || CL) ? cirow[j][h] : 0.0;
-          if constexpr (OPK != KM_OP_NONE && (CU || CL)) {
-            if (with_op) apply_op_fast<OPK>(op, octx, lf, col, re, im);
-          }
-          dst[p] = narrow<TO>(re, im);
+          fn(dst, obj + static_cast<int64_t>(col) * cs, j, h, col);
         }
       }
     };
+    // accumulate-into-output (sp.acc): row i's accumulators += the stored values, as
+    // numpy's `out += product` (the product rounded to f64 first: it is exact in the
+    // accumulator), before any fused op sees them
+    auto accum_row = [&](const int i, double (&crow)[4][2], double (&cirow)[4][2]) {
+      visit_row(i, [&](TO* dst, int64_t p, int j, int h, int) {
+        double re = crow[j][h], im = (CU || CL) ? cirow[j][h] : 0.0;
+        add_old(dst[p], re, im);
+        crow[j][h] = re;
+        if constexpr (CU || CL) cirow[j][h] = im;
+      });
+    };
+    // one 8-row block of the warp tile: row i (runtime) with accumulators crow/cirow
+    // (with_op false: the values were already transformed, gpe_rows below)
+    auto emit_row = [&](const int i, const double (&crow)[4][2], const double (&cirow)[4][2], const bool with_op) {
+      const int64_t f = m0 + wm + i * 8 + g;
+      const double lf = (with_op && f < M) ? split_fiber_weight<OPK>(op, f) : 0.0;
+      visit_row(i, [&](TO* dst, int64_t p, int j, int h, int col) {
+        double re = crow[j][h], im = (CU || CL) ? cirow[j][h] : 0.0;
+        if (with_op && sp.acc) add_old(dst[p], re, im);  // (other paths ran accum_row already)
+        if constexpr (OPK != KM_OP_NONE && (CU || CL)) {
+          if (with_op) apply_op_fast<OPK>(op, octx, lf, col, re, im);
+        }
+        dst[p] = narrow<TO>(re, im);
+      });
+    };
     if constexpr (OPK == KM_OP_NONE) {
+      if (sp.acc) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) accum_row(i, cr[i], ci[i]);
+      }
 #pragma unroll
       for (int i = 0; i < 4; ++i) emit_row(i, cr[i], ci[i], false);
     } else if constexpr (OPK == KM_OP_GPE_PHASE && (CU || CL)) {
@@ -453,6 +476,7 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
       for (int i = 0; i < 4; ++i) {
         const int64_t f = m0 + wm + i * 8 + g;
         const double lf = f < M ? split_fiber_weight<OPK>(op, f) : 1.0;
+        if (sp.acc) accum_row(i, cr[0], ci[0]);
         constexpr int EV = KMB_EPI_VEC;  // elements per gpe_rotate_vec call
 #pragma unroll
         for (int hv = 0; hv < 8 / EV; ++hv) {

@@ -77,16 +77,18 @@ class LocalStepper:
 
 class Prod:
     """One product of a slab schedule: direction ``mu`` with matrix ``mat`` (a key of the
-    stepper's matrices: "E1", "E2", "E3", "E3p", "E3r0", "E3r1") of ``m`` rows, the
+    stepper's matrices: "E1", "E2", "E3", "E3p0", "E3p1", "E3r0", "E3r1") of ``m`` rows, the
     (n_left, n_mu, n_right) flattening, the blocked input / output (km_mumode_split) and the
     source / destination buffers ("a", "w", "send", "recv") with element offsets."""
 
-    __slots__ = ("mu", "mat", "m", "nl", "nmu", "nr", "kcb", "kbs", "ncb", "nbs", "src", "soff", "dst", "doff")
+    __slots__ = ("mu", "mat", "m", "nl", "nmu", "nr", "kcb", "kbs", "ncb", "nbs", "src", "soff", "dst", "doff",
+                 "acc")
 
-    def __init__(self, mu, mat, m, nl, nmu, nr, kcb, kbs, ncb, nbs, src, soff, dst, doff):
+    def __init__(self, mu, mat, m, nl, nmu, nr, kcb, kbs, ncb, nbs, src, soff, dst, doff, acc=0):
         self.mu, self.mat, self.m, self.nl, self.nmu, self.nr = mu, mat, m, nl, nmu, nr
         self.kcb, self.kbs, self.ncb, self.nbs = kcb, kbs, ncb, nbs
         self.src, self.soff, self.dst, self.doff = src, soff, dst, doff
+        self.acc = acc  # 1: accumulate into the destination (km_mumode_split accumulate)
 
     def plain_out(self):
         return self.ncb == self.m
@@ -150,8 +152,10 @@ class SlabPlan:
 
         * even (A -> B): direction 2 on the i3-halves of the slab (n_right = c3/2), per-peer
           blocks of (n1, c2, c3/2); the receive buffer holds block (h, source q) at
-          ``(h*P + q) * bs/2``, which direction 3 reads as ONE blocked input (in_block = c3/2)
-          against E3 with its columns permuted to that order (``E3p``);
+          ``(h*P + q) * bs/2``.  Direction 3 contracts over i3, so it splits the same way:
+          half h of its sum reads receive half h as a blocked input (in_block = c3/2) against
+          the matching columns of E3 (``E3p0`` / ``E3p1``), the second half accumulating into
+          the first's output — half 0's part runs while half 1 is still moving;
         * odd (B -> A): direction 1, then direction 3 in two halves of output rows (``E3r0`` /
           ``E3r1``: the rows of E3 whose i3 lie in the first / second half of every peer's
           chunk), per-peer blocks of (n1, c2, c3/2); direction 2 then runs per half (i3 of
@@ -174,7 +178,8 @@ class SlabPlan:
             pre = [[Prod(0, "E1", n1, 1, n1, n2 * c3, n1, 0, n1, 0, "a", 0, "w", 0),
                     Prod(1, "E2", n2, n1, n2, h3, n2, 0, c2, bsh, "w", 0, "send", 0)],
                    [Prod(1, "E2", n2, n1, n2, h3, n2, 0, c2, bsh, "w", n1 * n2 * h3, "send", P * bsh)]]
-            post = [[], [Prod(2, "E3p", n3, n1 * c2, n3, 1, h3, bsh, n3, 0, "recv", 0, "a", 0)]]
+            post = [[Prod(2, "E3p0", n3, n1 * c2, n3 // 2, 1, h3, bsh, n3, 0, "recv", 0, "a", 0)],
+                    [Prod(2, "E3p1", n3, n1 * c2, n3 // 2, 1, h3, bsh, n3, 0, "recv", P * bsh, "a", 0, acc=1)]]
         else:
             pre = [[Prod(0, "E1", n1, 1, n1, c2 * n3, n1, 0, n1, 0, "a", 0, "w", 0),
                     Prod(2, "E3r0", n3 // 2, n1 * c2, n3, 1, n3, 0, h3, bsh, "w", 0, "send", 0)],
@@ -183,10 +188,10 @@ class SlabPlan:
                     [Prod(1, "E2", n2, n1, n2, h3, c2, bsh, n2, 0, "recv", P * bsh, "a", n1 * n2 * h3)]]
         return pre, post, P * bsh
 
-    def e3_column_order(self):
-        """pi: column k' of E3p is column pi[k'] of E3 (the even-step receive order)."""
+    def e3_column_halves(self):
+        """pi_h: column k' of E3p<h> is column pi_h[k'] of E3 (the even-step receive order of half h)."""
         P, c3, h3 = self.P, self.c3, self.c3 // 2
-        return np.array([q * c3 + h * h3 + j for h in range(2) for q in range(P) for j in range(h3)])
+        return [np.array([q * c3 + h * h3 + j for q in range(P) for j in range(h3)]) for h in range(2)]
 
     def e3_row_halves(self):
         """rho_g: row i' of E3r<g> is row rho_g[i'] of E3 (the odd-step send order)."""
@@ -244,14 +249,15 @@ class SlabStepper:
         self.derived = {}
         if self.overlap:
             self._derive(self.mats[2])
-        self.launches_per_step = 4 if self.overlap else 3
+        self.launches_per_step = 5 if self.overlap else 3
         self._works = []
 
     def _derive(self, e3):
-        """E3 with permuted columns (even steps) and its two row halves (odd steps)."""
+        """E3's two column halves in the even-step receive order and its two row halves in the
+        odd-step send order (contiguous row-major copies, as the kernels read factors)."""
         torch = dv.torch
-        pi = torch.as_tensor(self.plan.e3_column_order(), device=e3.device)
-        self.derived["E3p"] = e3.index_select(1, pi).contiguous()
+        for h, pi in enumerate(self.plan.e3_column_halves()):
+            self.derived[f"E3p{h}"] = e3.index_select(1, torch.as_tensor(pi, device=e3.device)).contiguous()
         for g, rho in enumerate(self.plan.e3_row_halves()):
             self.derived[f"E3r{g}"] = e3.index_select(0, torch.as_tensor(rho, device=e3.device)).contiguous()
 
@@ -286,7 +292,7 @@ class SlabStepper:
             _native.check(self.lib.km_mumode_split(
                 self._buf(p.src).data_ptr() + es * p.soff, self.code, mat.data_ptr(), self.mcodes[p.mu],
                 self._buf(p.dst).data_ptr() + es * p.doff, p.m, p.nl, p.nmu, p.nr, p.kcb, p.kbs, p.ncb, p.nbs,
-                ctypes.byref(post) if fuse else None, stream))
+                p.acc, ctypes.byref(post) if fuse else None, stream))
             if fuse:
                 post = None
         if post is not None:
@@ -455,9 +461,9 @@ class SlabTdpotStepper(SlabStepper):
         # the derived forms of E3 (permuted columns, row halves) are folded per step from their
         # own unfolded copies, with the node vector permuted the same way
         self.base = {k: v.clone() for k, v in self.derived.items()}
-        self.x_perm = None
         if self.overlap:
-            self.x_perm = self.x.index_select(0, torch.as_tensor(plan.e3_column_order(), device=self.x.device))
+            self.x_cols = [self.x.index_select(0, torch.as_tensor(c, device=self.x.device))
+                           for c in plan.e3_column_halves()]
             self.x_rows = [self.x.index_select(0, torch.as_tensor(r, device=self.x.device))
                            for r in plan.e3_row_halves()]
         self.launches_per_step += 1
@@ -474,8 +480,9 @@ class SlabTdpotStepper(SlabStepper):
         if not self.overlap:
             self._fold(self.e3, self.folded, self.x, self.x, c_a, c_b)
             self.mats[2] = self.folded
-        elif self.layout == "A":  # even step: E3 with permuted columns
-            self._fold(self.base["E3p"], self.derived["E3p"], self.x, self.x_perm, c_a, c_b)
+        elif self.layout == "A":  # even step: the two column halves
+            for h in range(2):
+                self._fold(self.base[f"E3p{h}"], self.derived[f"E3p{h}"], self.x, self.x_cols[h], c_a, c_b)
         else:  # odd step: the two row halves
             for g in range(2):
                 self._fold(self.base[f"E3r{g}"], self.derived[f"E3r{g}"], self.x_rows[g], self.x, c_a, c_b)

@@ -268,6 +268,36 @@ def run_tucker(u, mats, pre=None, post=None, out_dtype=None, keepalive=()):
     return _finish(uo, out, result, cdt)
 
 
+def kronecker_sum_apply(t, mats, out=None):
+    """``sum_mu t x_mu mats[mu]`` on the device in d launches (kron.py:94-102).
+
+    ``t`` is a column-major CUDA tensor and ``mats`` square device matrices, all
+    of one precision; the first product writes ``out`` (column-major, the
+    promoted dtype), every later one accumulates into it in its epilogue
+    (km_mumode_split accumulate = 1: ``out += p`` rounded as numpy does), so the
+    sum costs no extra HBM pass and no temporary.  A real tensor with complex
+    factors is widened first (every term must be of the output dtype).
+    """
+    lib = _native.lib()
+    shape = tuple(t.shape)
+    dev = t.device
+    cdt = np.result_type(dv.np_dtype(t.dtype), *[dv.np_dtype(m.dtype) for m in mats])
+    if dv.np_dtype(t.dtype) != cdt:
+        t = dv.tensor_as(t, cdt)
+    t = dv.as_fortran(t)
+    if out is None:
+        out = dv.fortran_empty(shape, dv.torch_dtype(cdt), dev)
+    stream = dv.stream_ptr(dev)
+    code = dv.code(cdt)
+    for mu, m in enumerate(mats):
+        n = shape[mu]
+        nl, nr = prod(shape[:mu]), prod(shape[mu + 1:])
+        _tally(n * prod(shape))
+        _native.check(lib.km_mumode_split(t.data_ptr(), code, m.data_ptr(), dv.code(dv.np_dtype(m.dtype)),
+                                          out.data_ptr(), n, nl, n, nr, n, 0, n, 0, 1 if mu else 0, None, stream))
+    return out
+
+
 def _finish(uo, out, result, cdt):
     if uo.is_tensor and uo.obj.is_cuda:
         if result != cdt:

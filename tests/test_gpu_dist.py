@@ -39,7 +39,7 @@ def test_split_kernel_addressing():
     L_d = torch.from_numpy(np.ascontiguousarray(L)).to(dev)
     _native.check(_native.lib().km_mumode_split(
         src_d.data_ptr(), _native.KM_C128, L_d.data_ptr(), _native.KM_C128, out_d.data_ptr(),
-        m, nl, nmu, nr, kcb, kbs, ncb, nbs, None, dv.stream_ptr(dev)))
+        m, nl, nmu, nr, kcb, kbs, ncb, nbs, 0, None, dv.stream_ptr(dev)))
     out = out_d.cpu().numpy()
     got = np.concatenate([out[b * nbs: b * nbs + nl * ncb * nr].reshape((nl, ncb, nr), order="F")
                           for b in range(m // ncb)], axis=1)
@@ -49,8 +49,8 @@ def test_split_kernel_addressing():
 def test_split_rejects_bad_blocks():
     lib = _native.lib()
     p = ctypes.c_void_p(16)
-    assert lib.km_mumode_split(p, 3, p, 3, p, 16, 4, 20, 2, 10, 40, 16, 0, None, None) == _native.KM_EINVAL
-    assert lib.km_mumode_split(p, 3, p, 3, p, 16, 1, 32, 2, 16, 64, 16, 0, None, None) == _native.KM_EINVAL
+    assert lib.km_mumode_split(p, 3, p, 3, p, 16, 4, 20, 2, 10, 40, 16, 0, 0, None, None) == _native.KM_EINVAL
+    assert lib.km_mumode_split(p, 3, p, 3, p, 16, 1, 32, 2, 16, 64, 16, 0, 0, None, None) == _native.KM_EINVAL
 
 
 @pytest.mark.parametrize("P,n,steps,exchange,overlap", [

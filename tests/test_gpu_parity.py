@@ -490,3 +490,29 @@ def test_norms_large_vs_numpy(kind):
     w = ws if kind == "weighted_two" else None
     assert km.norm(u, kind, w) == pytest.approx(want_n, rel=1e-13)
     assert km.relative_error(u, ref, kind, w) == pytest.approx(want_e, rel=1e-12)
+
+
+@pytest.mark.parametrize("dtype,tol", [(np.complex128, 0.0), (np.float64, 0.0), (np.complex64, 1e-5)])
+def test_matvec_accumulates_like_the_reference(dtype, tol):
+    """kron.matvec accumulates the d products in the epilogues (km_mumode_split accumulate):
+    the same ``out += p`` roundings as kron.py:99-101 (bitwise in double precision against
+    the oracle's products summed the reference's way), 3 launches, no temporaries."""
+    rng = np.random.default_rng(21)
+    shape = (48, 40, 36)
+    cplx = np.dtype(dtype).kind == "c"
+    u = crand(rng, shape, dtype) if cplx else np.asfortranarray(rng.standard_normal(shape).astype(dtype))
+    facs = [rng.standard_normal((n, n)).astype(dtype) + (1j * rng.standard_normal((n, n)) if cplx else 0)
+            for n in shape]
+    facs = [f.astype(dtype) for f in facs]
+    op = km.KroneckerOp(tuple(facs))
+    got = km.matvec(op, u)
+    want = km.mu_mode_product(u, facs[0], 1)
+    for mu in (2, 3):
+        want = want + km.mu_mode_product(u, facs[mu - 1], mu)
+    assert got.dtype == want.dtype
+    if tol == 0.0:
+        assert np.array_equal(got, want)
+    ref = orc.mu_mode_product(u, facs[0], 1)
+    for mu in (2, 3):
+        ref += orc.mu_mode_product(u, facs[mu - 1], mu)
+    assert rel(got, ref) <= (1e-12 if tol == 0.0 else tol)

@@ -54,7 +54,8 @@ class CpuSlabStepper(dist.SlabStepper):
         self._works = []
 
     def _derive(self, e3):
-        self.derived["E3p"] = e3[:, self.plan.e3_column_order()]
+        for h, pi in enumerate(self.plan.e3_column_halves()):
+            self.derived[f"E3p{h}"] = e3[:, pi]
         for g, rho in enumerate(self.plan.e3_row_halves()):
             self.derived[f"E3r{g}"] = e3[rho, :]
 
@@ -68,6 +69,8 @@ class CpuSlabStepper(dist.SlabStepper):
             dst = self._np(p.dst)[p.doff:]
             x = gather_in(src, p.nl, p.nmu, p.nr, p.kcb, p.kbs)
             y = orc.mu_mode_product(x, self._mat(p.mat), 2)
+            if p.acc:
+                y = gather_in(dst, p.nl, p.m, p.nr, p.m, 0) + y
             scatter_out(dst, y, p.ncb, p.nbs)
         if post is not None:
             self._phase(self.a, post)

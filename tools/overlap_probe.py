@@ -14,8 +14,8 @@ numbers per case:
   an HBM copy;
 * model: compute + the exposed part of an exchange at NVLink speed (the measured
   770 GB/s peer bandwidth), from the per-group times: serial exposes
-  all of it; the two-half schedule hides half 0 under the half-1 products and, on
-  odd steps, half 1 under the first post product.
+  all of it; the two-half schedule hides half 0 under the half-1 products and
+  half 1 under the first post group (half 0's share of the post products).
 
 One GPU stands in for rank 0 only; no kernel waits on another rank's work.
 """
@@ -106,8 +106,8 @@ def model(gt, overlap, es=16):
         if not overlap:
             tot += comp + x
             continue
-        # half 0 moves during the half-1 pre products; half 1 during post group 0 (odd steps)
-        exposed = max(0.0, x - pre[1]) + max(0.0, x - max(0.0, post[0]))
+        # half 0 moves during the half-1 pre products; half 1 during post group 0
+        exposed = max(0.0, x - pre[1]) + max(0.0, x - post[0])
         tot += comp + exposed
     return tot / 2
 
