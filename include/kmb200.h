@@ -240,6 +240,23 @@ int km_tucker(const void* u, int u_dtype, int d, const int64_t* dims,
               void* out, void* ws0, void* ws1,
               const km_pointop* pre, const km_pointop* post, void* stream);
 
+/*
+ * `steps` exact steps of a complex128 n1 x n2 x n3 state in ONE persistent
+ * launch (reference: kron.step, kron.py:110-121, applied `steps` times; the
+ * time loop of problems.py:597-598): the d = 3 sweeps of every step run as
+ * one dataflow of 32 x 32 tiles whose dependencies on the previous sweep are
+ * tracked by counters, so the sweeps overlap instead of paying a launch,
+ * a pipeline fill and a partial last wave each (small, L2-resident states).
+ * E1..E3 are the row-major n_mu x n_mu complex128 propagators; `state` is
+ * updated in place.  Extents must be multiples of 32 in [32, 96]
+ * (KM_EINVAL otherwise; the caller then steps with km_tucker).  The
+ * workspace (two state copies + counters) is km_steps_small_workspace_bytes.
+ * Not capturable into a CUDA graph (cooperative launch).
+ */
+int km_steps_small_workspace_bytes(int64_t n1, int64_t n2, int64_t n3, int64_t steps, size_t* bytes);
+int km_steps_small(void* state, const void* E1, const void* E2, const void* E3, int64_t n1, int64_t n2,
+                   int64_t n3, int64_t steps, void* workspace, size_t workspace_bytes, void* stream);
+
 /* bytes each of ws0/ws1 needs for km_tucker with these arguments */
 int km_tucker_workspace(int u_dtype, int d, const int64_t* dims, const void* const* mats,
                         const int* mat_dtypes, const int64_t* rows, size_t* bytes);

@@ -45,6 +45,8 @@ EXPORTS = (
     "km_norm_workspace_bytes",
     "km_norm",
     "km_stream_workspace_bytes",
+    "km_steps_small_workspace_bytes",
+    "km_steps_small",
     "km_set_stream_workspace",
 )
 
@@ -112,6 +114,10 @@ def _declare(lib):
     lib.km_norm.argtypes = [c_vp, c_vp, c_int, c_i64, c_int, p_op, c_vp, c_vp, c_sz, c_vp]
     lib.km_set_kernel_policy.restype = c_int
     lib.km_set_kernel_policy.argtypes = [c_int]
+    lib.km_steps_small_workspace_bytes.restype = c_int
+    lib.km_steps_small_workspace_bytes.argtypes = [c_i64, c_i64, c_i64, c_i64, ctypes.POINTER(c_sz)]
+    lib.km_steps_small.restype = c_int
+    lib.km_steps_small.argtypes = [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_sz, c_vp]
     lib.km_stream_workspace_bytes.restype = c_int
     lib.km_stream_workspace_bytes.argtypes = [ctypes.POINTER(c_sz)]
     lib.km_set_stream_workspace.restype = c_int

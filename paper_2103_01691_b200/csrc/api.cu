@@ -19,6 +19,9 @@ extern bool g_tc_halves_disabled;  // inst_tc32_c64.cu
 size_t tc32_workspace_bytes(int64_t m, int64_t K);  // inst_tc32_c64.cu
 size_t streamk_workspace_bytes();                    // inst_tma_c128.cu
 int bind_streamk_workspace(cudaStream_t st, void* ws, size_t bytes);  // inst_tma_c128.cu
+int steps_small_workspace(int64_t n1, int64_t n2, int64_t n3, int64_t steps, size_t* bytes);  // inst_small.cu
+int launch_steps_small(void* state, const void* E1, const void* E2, const void* E3, int64_t n1, int64_t n2,
+                       int64_t n3, int64_t steps, void* ws, size_t ws_bytes, cudaStream_t st);  // inst_small.cu
 int launch_tc32_c64(const void* u, const void* L, void* out, int64_t m, int64_t nl, int64_t K, int64_t nr, void* ws,
                     size_t ws_bytes, cudaStream_t st);
 thread_local char g_err[512] = "";
@@ -367,6 +370,16 @@ int km_mumode_split(const void* u, int u_dtype, const void* L, int L_dtype, void
   sp.acc = accumulate;
   return mumode_impl(u, u_dtype, L, L_dtype, out, m, n_left, n_mu, n_right, post,
                      static_cast<cudaStream_t>(stream), &sp);
+}
+
+int km_steps_small_workspace_bytes(int64_t n1, int64_t n2, int64_t n3, int64_t steps, size_t* bytes) {
+  return steps_small_workspace(n1, n2, n3, steps, bytes);
+}
+
+int km_steps_small(void* state, const void* E1, const void* E2, const void* E3, int64_t n1, int64_t n2, int64_t n3,
+                   int64_t steps, void* workspace, size_t workspace_bytes, void* stream) {
+  return launch_steps_small(state, E1, E2, E3, n1, n2, n3, steps, workspace, workspace_bytes,
+                            static_cast<cudaStream_t>(stream));
 }
 
 int km_stream_workspace_bytes(size_t* bytes) {

@@ -1,0 +1,254 @@
+// mumode_steps_kernel — many exact steps of a small (L2-resident) complex128
+// cube in ONE persistent launch: the d = 3 sweeps of every step fused into a
+// dataflow of tiles with fine-grained dependency counters instead of one
+// launch (or one grid barrier) per product.
+//
+// Reference: kron.step (kron.py:110-121) = tucker (tensor.py:143-166) applied
+// `steps` times, i.e. the product chain ×_1 E_1 ×_2 E_2 ×_3 E_3 ×_1 E_1 ...
+// (the loop of problems.py:597-598 / the config-1 benchmark).
+//
+// Why: at 64³ one product is 3.6 µs of DMMA work, but a per-product launch
+// pays its pipeline fill, its 1.73-wave tile quantisation (256 tiles on 148
+// SMs) and the launch gap every time (0.50 of the DMMA peak in a CUDA graph,
+// DESIGN.md §2.5).  Here the tiles of all 3·steps products form one ordered
+// list; CTA c (of G persistent CTAs, 2–3 per SM) takes tiles c, c+G, c+2G, ...
+// A tile of product p waits only for the tiles of product p-1 it reads
+// (counters per dependency group), so the next product's first tiles run in
+// the current product's last partial wave.
+//
+// Tiles: 32 fibers × 32 output rows × the whole contraction (K = n_mu ≤ 96),
+// staged in one shot with cp.async (the state is in L2).  The fibers of a tile
+// are 32 consecutive indices of the faster "other" direction at one fixed
+// index of the slower one:
+//   dir 1: i2-block a, i3 = b      dir 2: i1-block a, i3 = b      dir 3: i1-block a, i2 = b
+// Dependency groups (the producer tiles a consumer reads, all of them one
+// counter):
+//   dir 2 tile (a, b=i3)  <- dir 1 tiles with i3 = b, row block = a         (n2/32 tiles)
+//   dir 3 tile (a, b=i2)  <- dir 2 tiles with i1-block a, row block b/32    (n3 tiles)
+//   dir 1 tile (a, b=i3)  <- dir 3 tiles with i2-block a, row block b/32    (n1 tiles)
+// Buffers rotate over three (product p reads buf[p%3], writes buf[(p+1)%3]);
+// buf[0] is the state, so after 3·steps products the result is back in it.
+// Before writing, a tile also waits until product p-2 (the last reader of its
+// destination) is complete — write-after-read safety, normally long satisfied.
+//
+// Deadlock freedom: every dependency points to an earlier tile of the list,
+// each CTA walks its tiles in list order, and the cooperative launch makes all
+// CTAs co-resident; so the earliest unfinished tile always has its inputs.
+#pragma once
+#include "kmb200_kernels.cuh"
+
+namespace kmb {
+namespace sm {
+
+constexpr int BT = 32;          // tile edge: fibers and output rows
+constexpr int THREADS = 128;    // 4 warps, 2 x 2 warp tiles of 16 x 16
+constexpr int KMAX = 96;        // largest contraction staged in one shot
+constexpr int CNT_STRIDE = 512; // counters per product (groups + the total)
+
+struct Params {
+  double2* buf[3];        // buf[0]: the state (in / out); buf[1], buf[2]: workspace
+  const double2* E[3];    // row-major n_mu x n_mu factors
+  int n[3];
+  int products;           // 3 * steps
+  unsigned* cnt;          // products x CNT_STRIDE counters, zeroed before the launch
+};
+
+__host__ __device__ inline int smem_bytes(int kmax) { return 2 * BT * (kmax + 4) * 16; }
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void wait_count(const unsigned* p, unsigned need) {
+  long long spins = 0;
+  while (ld_acquire(p) < need) {
+    __nanosleep(32);
+    if (++spins > (1ll << 28)) __trap();  // a lost producer must not hang the device
+  }
+}
+
+// tiles of one product of direction mu, and (a, b, r) of its t-th tile in list order
+struct TileMap {
+  int mu, na, nb, nr;  // a-blocks, b values, row blocks
+  // (ternaries, not P.n[runtime index]: a dynamically indexed kernel parameter is
+  // copied to local memory)
+  __device__ TileMap(const Params& P, int mu_) : mu(mu_) {
+    const int n1 = P.n[0], n2 = P.n[1], n3 = P.n[2];
+    na = (mu == 0 ? n2 : n1) / BT;  // faster other direction
+    nb = mu == 2 ? n2 : n3;         // slower other direction
+    nr = (mu == 0 ? n1 : mu == 1 ? n2 : n3) / BT;
+  }
+  __device__ int count() const { return na * nb * nr; }
+  // order: direction 1 b-major (i3 outer), directions 2 and 3 a-major (i1-block outer);
+  // row blocks innermost, so a producer group's tiles are consecutive where possible
+  __device__ void decode(int t, int& a, int& b, int& r) const {
+    r = t % nr;
+    const int q = t / nr;
+    if (mu == 0) {
+      a = q % na;
+      b = q / na;
+    } else {
+      b = q % nb;
+      a = q / nb;
+    }
+  }
+};
+
+__global__ void __launch_bounds__(THREADS) mumode_steps_kernel(const Params P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int wm = (warp & 1) * 16, wn = (warp >> 1) * 16;
+  const int n1 = P.n[0], n2 = P.n[1], n3 = P.n[2];
+
+  // list position of this CTA: product p, tile index within it
+  int p = 0, ti = blockIdx.x;
+  while (p < P.products) {
+    const int mu = p % 3;
+    const TileMap tm(P, mu);
+    const int cnt_p = tm.count();
+    if (ti >= cnt_p) {  // past this product: carry over into the next one
+      ti -= cnt_p;
+      ++p;
+      continue;
+    }
+    int a, b, r;
+    tm.decode(ti, a, b, r);
+    const int K = mu == 0 ? n1 : mu == 1 ? n2 : n3;
+    const int PK = K + 4;  // smem pitch in complex elements (conflict-free fragment reads)
+    double2* As = reinterpret_cast<double2*>(smem);
+    double2* Bs = As + BT * PK;
+
+    // global addressing: element (j, k) of the A tile and (j, i) of the output at
+    // base + j * sa + k * sk (the output has the input's shape: square factors)
+    int64_t base, sa, sk;
+    if (mu == 0) {
+      base = (static_cast<int64_t>(a) * BT + static_cast<int64_t>(n2) * b) * n1;
+      sa = n1;
+      sk = 1;
+    } else if (mu == 1) {
+      base = static_cast<int64_t>(a) * BT + static_cast<int64_t>(b) * n1 * n2;
+      sa = 1;
+      sk = n1;
+    } else {
+      base = static_cast<int64_t>(a) * BT + static_cast<int64_t>(n1) * b;
+      sa = 1;
+      sk = static_cast<int64_t>(n1) * n2;
+    }
+    const int pi = p % 3;
+    const double2* __restrict__ src = pi == 0 ? P.buf[0] : pi == 1 ? P.buf[1] : P.buf[2];
+    double2* __restrict__ dst = pi == 0 ? P.buf[1] : pi == 1 ? P.buf[2] : P.buf[0];
+    const double2* __restrict__ E = mu == 0 ? P.E[0] : mu == 1 ? P.E[1] : P.E[2];
+
+    // 1. the factor rows of this tile (independent of the dependencies)
+    for (int e = tid; e < BT * K; e += THREADS) {
+      const int i = e / K, k = e - i * K;
+      cp_async<16>(Bs + i * PK + k, E + static_cast<int64_t>(r * BT + i) * K + k, true);
+    }
+    cp_commit();
+
+    // 2. the producer group of this tile, and the last reader of its destination
+    if (tid == 0) {
+      if (p >= 1) {
+        const unsigned* c = P.cnt + static_cast<int64_t>(p - 1) * CNT_STRIDE;
+        int grp;
+        unsigned need;
+        if (mu == 1) {         // dir 1 tiles with i3 = b, row block a
+          grp = b * (n1 / BT) + a;
+          need = n2 / BT;
+        } else if (mu == 2) {  // dir 2 tiles with i1-block a, row block b / 32
+          grp = a * (n2 / BT) + b / BT;
+          need = n3;
+        } else {               // dir 3 tiles with i2-block a, row block b / 32
+          grp = a * (n3 / BT) + b / BT;
+          need = n1;
+        }
+        wait_count(c + grp, need);
+      }
+      if (p >= 2) {
+        const TileMap t2(P, (p - 2) % 3);
+        wait_count(P.cnt + static_cast<int64_t>(p - 2) * CNT_STRIDE + (CNT_STRIDE - 1), t2.count());
+      }
+    }
+    __syncthreads();
+
+    // 3. the A tile (32 fibers x K): k fastest for direction 1, fibers fastest otherwise
+    if (mu == 0) {
+      for (int e = tid; e < BT * K; e += THREADS) {
+        const int j = e / K, k = e - j * K;
+        cp_async<16>(As + j * PK + k, src + base + j * sa + k, true);
+      }
+    } else {
+      for (int e = tid; e < BT * K; e += THREADS) {
+        const int j = e & (BT - 1), k = e >> 5;
+        cp_async<16>(As + j * PK + k, src + base + j + k * sk, true);
+      }
+    }
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+
+    // 4. the tile's products: 2 x 2 DMMA tiles of 8 x 8 per warp, complex x complex
+    double cr[2][2][2], ci[2][2][2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) {
+        cr[x][y][0] = cr[x][y][1] = 0.0;
+        ci[x][y][0] = ci[x][y][1] = 0.0;
+      }
+#pragma unroll 4
+    for (int kk = 0; kk < K; kk += 4) {
+      double2 av[2], bv[2];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) av[x] = As[(wm + x * 8 + g) * PK + kk + t];
+#pragma unroll
+      for (int y = 0; y < 2; ++y) bv[y] = Bs[(wn + y * 8 + g) * PK + kk + t];
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 2; ++y) {
+          dmma(cr[x][y][0], cr[x][y][1], av[x].x, bv[y].x);
+          dmma(ci[x][y][0], ci[x][y][1], av[x].x, bv[y].y);
+        }
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 2; ++y) {
+          dmma(cr[x][y][0], cr[x][y][1], av[x].y, negate(bv[y].y));
+          dmma(ci[x][y][0], ci[x][y][1], av[x].y, bv[y].x);
+        }
+    }
+
+    // 5. store: C fragment (g, 2t + h) of each 8x8 tile -> (fiber j, row i)
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = wm + x * 8 + g;
+          const int i = r * BT + wn + y * 8 + 2 * t + h;
+          dst[base + j * sa + static_cast<int64_t>(i) * sk] = make_double2(cr[x][y][h], ci[x][y][h]);
+        }
+    __threadfence();
+    __syncthreads();  // every store of the tile (and every smem read) is done
+
+    // 6. publish: the consumer group this tile belongs to, and the product's total
+    if (tid == 0) {
+      unsigned* c = P.cnt + static_cast<int64_t>(p) * CNT_STRIDE;
+      int grp;
+      if (mu == 0) grp = b * (n1 / BT) + r;            // (i3, i1-block) for dir 2
+      else if (mu == 1) grp = a * (n2 / BT) + r;       // (i1-block, i2-block) for dir 3
+      else grp = (b / BT) * (n3 / BT) + r;             // (i2-block, i3-block) for dir 1
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(c + grp) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(c + CNT_STRIDE - 1) : "memory");
+    }
+    ti += gridDim.x;
+  }
+}
+
+}  // namespace sm
+}  // namespace kmb

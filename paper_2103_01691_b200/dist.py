@@ -50,6 +50,35 @@ class LocalStepper:
             None if self.post is None else ctypes.byref(self.post), stream))
         self.a, self.b = self.b, self.a
 
+    def run(self, steps):
+        """``steps`` exact steps.  A complex128 3D state whose extents are multiples of 32 up
+        to 96 (L2-resident: configuration 1) runs them as ONE persistent launch
+        (``km_steps_small``: the 3·steps sweeps as a dataflow of tiles, no per-product
+        launch, fill or partial wave); any other state steps one ``km_tucker`` at a time."""
+        if steps < 1:
+            return
+        ws = self._steps_workspace(steps)
+        if ws is None:
+            for _ in range(steps):
+                self.step()
+            return
+        _native.check(self.lib.km_steps_small(
+            self.a.data_ptr(), self.mats[0].data_ptr(), self.mats[1].data_ptr(), self.mats[2].data_ptr(),
+            *self.dims, steps, ws.data_ptr(), ws.numel(), dv.stream_ptr(self.a.device)))
+
+    def _steps_workspace(self, steps):
+        torch = self.torch
+        if (self.d != 3 or self.pre is not None or self.post is not None or self.a.dtype != torch.complex128
+                or not dv.is_fortran(self.a)
+                or any(m.dtype != torch.complex128 or tuple(m.shape) != (n, n) for m, n in zip(self.mats, self.dims))):
+            return None
+        nbytes = ctypes.c_size_t(0)
+        if self.lib.km_steps_small_workspace_bytes(*self.dims, steps, ctypes.byref(nbytes)) != _native.KM_OK:
+            return None
+        if getattr(self, "_small_ws", None) is None or self._small_ws.numel() < nbytes.value:
+            self._small_ws = torch.empty(nbytes.value, dtype=torch.uint8, device=self.a.device)
+        return self._small_ws
+
     @property
     def state(self):
         return self.a
