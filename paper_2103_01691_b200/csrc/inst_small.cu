@@ -4,6 +4,10 @@
 
 namespace kmb {
 
+#ifdef KMB_STEPS_TRACE
+unsigned long long* g_steps_trace = nullptr;  // set by km_steps_small_trace (probe builds only)
+#endif
+
 namespace {
 bool steps_eligible(int64_t n1, int64_t n2, int64_t n3, int64_t steps) {
   const int64_t n[3] = {n1, n2, n3};
@@ -47,6 +51,10 @@ int launch_steps_small(void* state, const void* E1, const void* E2, const void* 
   P.n[2] = static_cast<int>(n3);
   P.products = static_cast<int>(3 * steps);
   P.cnt = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + 2 * sbytes);
+  P.trace = nullptr;
+#ifdef KMB_STEPS_TRACE
+  P.trace = g_steps_trace;
+#endif
   const size_t cbytes = static_cast<size_t>(P.products) * sm::CNT_STRIDE * sizeof(unsigned);
   cudaError_t e = cudaMemsetAsync(P.cnt, 0, cbytes, st);
   if (e != cudaSuccess) return fail(KM_ECUDA, "km_steps_small counters: %s", cudaGetErrorString(e));
@@ -57,8 +65,14 @@ int launch_steps_small(void* state, const void* E1, const void* E2, const void* 
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, sm::THREADS, smem) != cudaSuccess || per_sm < 1)
     return fail(KM_ECUDA, "km_steps_small: no resident CTA (%d B of shared memory)", smem);
-  // persistent: every co-resident CTA (a CTA past a product's tiles rolls into the next product)
-  const int grid = per_sm * num_sms();
+  // persistent, at most one CTA per tile of the largest product: CTA c then takes tile c of
+  // every product (more CTAs than tiles would queue a product's last tiles behind the
+  // previous product's on the same CTAs, measured: every product then costs two tile latencies)
+  const int64_t t1 = (n2 / sm::BT) * n3 * (n1 / sm::BT), t2 = (n1 / sm::BT) * n3 * (n2 / sm::BT),
+                t3 = (n1 / sm::BT) * n2 * (n3 / sm::BT);
+  const int64_t tmax = t1 > t2 ? (t1 > t3 ? t1 : t3) : (t2 > t3 ? t2 : t3);
+  const int64_t resident = static_cast<int64_t>(per_sm) * num_sms();
+  const int grid = static_cast<int>(tmax < resident ? tmax : resident);
   sm::Params* pp = &P;
   void* args[] = {pp};
   e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(sm::THREADS), args, smem, st);
@@ -67,3 +81,7 @@ int launch_steps_small(void* state, const void* E1, const void* E2, const void* 
 }
 
 }  // namespace kmb
+
+#ifdef KMB_STEPS_TRACE
+extern "C" void km_steps_small_trace(void* buf) { kmb::g_steps_trace = static_cast<unsigned long long*>(buf); }
+#endif

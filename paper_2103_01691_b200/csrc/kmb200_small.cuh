@@ -35,7 +35,7 @@
 // each CTA walks its tiles in list order, and the cooperative launch makes all
 // CTAs co-resident; so the earliest unfinished tile always has its inputs.
 #pragma once
-#include "kmb200_kernels.cuh"
+#include "kmb200_tma.cuh"
 
 namespace kmb {
 namespace sm {
@@ -51,9 +51,29 @@ struct Params {
   int n[3];
   int products;           // 3 * steps
   unsigned* cnt;          // products x CNT_STRIDE counters, zeroed before the launch
+  unsigned long long* trace;  // optional (KMB_STEPS_TRACE builds): 6 globaltimer stamps per tile
 };
 
-__host__ __device__ inline int smem_bytes(int kmax) { return 2 * BT * (kmax + 4) * 16; }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+constexpr int PM = BT + 2;      // pitch (complex elements) of the transposed A tile [k][fiber]
+
+// A (either [fiber][k] with pitch K+4, or [k][fiber] with pitch PM), B [row][k] with
+// pitch K+4, then two mbarriers
+__host__ __device__ inline int a_elems(int kmax) { return BT * (kmax + 4) > kmax * PM ? BT * (kmax + 4) : kmax * PM; }
+__host__ __device__ inline int smem_bytes(int kmax) { return (a_elems(kmax) + BT * (kmax + 4)) * 16 + 8 * (KMAX / BT); }
+
+// one contiguous global -> shared bulk copy (TMA engine, no tensor map), completing on bar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   tma::su32(dst)),
+               "l"(src), "r"(bytes), "r"(tma::su32(bar))
+               : "memory");
+}
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -103,6 +123,17 @@ __global__ void __launch_bounds__(THREADS) mumode_steps_kernel(const Params P) {
   const int wm = (warp & 1) * 16, wn = (warp >> 1) * 16;
   const int n1 = P.n[0], n2 = P.n[1], n3 = P.n[2];
 
+  const int kmax = n1 > n2 ? (n1 > n3 ? n1 : n3) : (n2 > n3 ? n2 : n3);
+  double2* As = reinterpret_cast<double2*>(smem);
+  double2* Bs = As + a_elems(kmax);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Bs + BT * (kmax + 4));
+  if (tid == 0) {
+    for (int c = 0; c < KMAX / BT; ++c) tma::mbar_init(&bars[c], 1);
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+  unsigned phases = 0;  // bit c: the parity chunk barrier c waits for next (each flips only when used)
+
   // list position of this CTA: product p, tile index within it
   int p = 0, ti = blockIdx.x;
   while (p < P.products) {
@@ -116,10 +147,21 @@ __global__ void __launch_bounds__(THREADS) mumode_steps_kernel(const Params P) {
     }
     int a, b, r;
     tm.decode(ti, a, b, r);
+#ifdef KMB_STEPS_TRACE
+    unsigned long long* tr = nullptr;
+    if (P.trace && tid == 0) {
+      int64_t gidx = ti;  // list index of this tile
+      for (int q = 0; q < p; ++q) gidx += TileMap(P, q % 3).count();
+      tr = P.trace + gidx * 6;
+      tr[0] = gtimer();
+      tr[5] = (static_cast<unsigned long long>(blockIdx.x) << 32) | static_cast<unsigned>(p);
+    }
+#define KMB_STAMP(i) if (tr) tr[i] = gtimer()
+#else
+#define KMB_STAMP(i)
+#endif
     const int K = mu == 0 ? n1 : mu == 1 ? n2 : n3;
     const int PK = K + 4;  // smem pitch in complex elements (conflict-free fragment reads)
-    double2* As = reinterpret_cast<double2*>(smem);
-    double2* Bs = As + BT * PK;
 
     // global addressing: element (j, k) of the A tile and (j, i) of the output at
     // base + j * sa + k * sk (the output has the input's shape: square factors)
@@ -142,53 +184,54 @@ __global__ void __launch_bounds__(THREADS) mumode_steps_kernel(const Params P) {
     double2* __restrict__ dst = pi == 0 ? P.buf[1] : pi == 1 ? P.buf[2] : P.buf[0];
     const double2* __restrict__ E = mu == 0 ? P.E[0] : mu == 1 ? P.E[1] : P.E[2];
 
-    // 1. the factor rows of this tile (independent of the dependencies)
-    for (int e = tid; e < BT * K; e += THREADS) {
-      const int i = e / K, k = e - i * K;
-      cp_async<16>(Bs + i * PK + k, E + static_cast<int64_t>(r * BT + i) * K + k, true);
-    }
-    cp_commit();
-
-    // 2. the producer group of this tile, and the last reader of its destination
-    if (tid == 0) {
-      if (p >= 1) {
-        const unsigned* c = P.cnt + static_cast<int64_t>(p - 1) * CNT_STRIDE;
-        int grp;
-        unsigned need;
-        if (mu == 1) {         // dir 1 tiles with i3 = b, row block a
-          grp = b * (n1 / BT) + a;
-          need = n2 / BT;
-        } else if (mu == 2) {  // dir 2 tiles with i1-block a, row block b / 32
-          grp = a * (n2 / BT) + b / BT;
-          need = n3;
-        } else {               // dir 3 tiles with i2-block a, row block b / 32
-          grp = a * (n3 / BT) + b / BT;
-          need = n1;
+    // 1-3: warp 0 stages the tile with bulk copies, one per lane: the factor rows at once,
+    // the A tile once its producers have published (k-contiguous fibers for direction 1,
+    // fiber-contiguous k-columns otherwise, stored transposed)
+    // staged in chunks of 32 k (one mbarrier each), so the MMAs of chunk 0 start while the
+    // later chunks are still in flight
+    const int nch = K / BT;
+    if (warp == 0) {
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // prior generic smem reads
+        for (int c = 0; c < nch; ++c) tma::mbar_expect_tx(&bars[c], 2 * BT * BT * 16);
+      }
+      __syncwarp();
+      for (int c = 0; c < nch; ++c)
+        bulk_g2s(Bs + lane * PK + c * BT, E + static_cast<int64_t>(r * BT + lane) * K + c * BT, BT * 16, &bars[c]);
+      if (lane == 0) {
+        if (p >= 1) {  // the producer group of this tile
+          const unsigned* cn = P.cnt + static_cast<int64_t>(p - 1) * CNT_STRIDE;
+          int grp;
+          unsigned need;
+          if (mu == 1) {         // dir 1 tiles with i3 = b, row block a
+            grp = b * (n1 / BT) + a;
+            need = n2 / BT;
+          } else if (mu == 2) {  // dir 2 tiles with i1-block a, row block b / 32
+            grp = a * (n2 / BT) + b / BT;
+            need = n3;
+          } else {               // dir 3 tiles with i2-block a, row block b / 32
+            grp = a * (n3 / BT) + b / BT;
+            need = n1;
+          }
+          wait_count(cn + grp, need);
         }
-        wait_count(c + grp, need);
+        if (p >= 2) {  // the last reader of this tile's destination
+          const TileMap t2(P, (p - 2) % 3);
+          wait_count(P.cnt + static_cast<int64_t>(p - 2) * CNT_STRIDE + (CNT_STRIDE - 1), t2.count());
+        }
+        KMB_STAMP(1);
       }
-      if (p >= 2) {
-        const TileMap t2(P, (p - 2) % 3);
-        wait_count(P.cnt + static_cast<int64_t>(p - 2) * CNT_STRIDE + (CNT_STRIDE - 1), t2.count());
-      }
-    }
-    __syncthreads();
-
-    // 3. the A tile (32 fibers x K): k fastest for direction 1, fibers fastest otherwise
-    if (mu == 0) {
-      for (int e = tid; e < BT * K; e += THREADS) {
-        const int j = e / K, k = e - j * K;
-        cp_async<16>(As + j * PK + k, src + base + j * sa + k, true);
-      }
-    } else {
-      for (int e = tid; e < BT * K; e += THREADS) {
-        const int j = e & (BT - 1), k = e >> 5;
-        cp_async<16>(As + j * PK + k, src + base + j + k * sk, true);
+      __syncwarp();
+      for (int c = 0; c < nch; ++c) {
+        if (mu == 0) {
+          bulk_g2s(As + lane * PK + c * BT, src + base + lane * sa + c * BT, BT * 16, &bars[c]);
+        } else {
+          const int k = c * BT + lane;
+          bulk_g2s(As + k * PM, src + base + k * sk, BT * 16, &bars[c]);
+        }
       }
     }
-    cp_commit();
-    cp_wait<0>();
-    __syncthreads();
+    if (tid == 0) KMB_STAMP(2);
 
     // 4. the tile's products: 2 x 2 DMMA tiles of 8 x 8 per warp, complex x complex
     double cr[2][2][2], ci[2][2][2];
@@ -199,11 +242,14 @@ __global__ void __launch_bounds__(THREADS) mumode_steps_kernel(const Params P) {
         cr[x][y][0] = cr[x][y][1] = 0.0;
         ci[x][y][0] = ci[x][y][1] = 0.0;
       }
+    // A fragment (fiber wm + 8x + g, k kk + t): [fiber][k] or [k][fiber]
+    const int a_row = mu == 0 ? PK : 1, a_col = mu == 0 ? 1 : PM;
 #pragma unroll 4
     for (int kk = 0; kk < K; kk += 4) {
+      if ((kk & (BT - 1)) == 0) tma::mbar_wait(&bars[kk / BT], (phases >> (kk / BT)) & 1u);
       double2 av[2], bv[2];
 #pragma unroll
-      for (int x = 0; x < 2; ++x) av[x] = As[(wm + x * 8 + g) * PK + kk + t];
+      for (int x = 0; x < 2; ++x) av[x] = As[(wm + x * 8 + g) * a_row + (kk + t) * a_col];
 #pragma unroll
       for (int y = 0; y < 2; ++y) bv[y] = Bs[(wn + y * 8 + g) * PK + kk + t];
 #pragma unroll
@@ -222,6 +268,8 @@ __global__ void __launch_bounds__(THREADS) mumode_steps_kernel(const Params P) {
         }
     }
 
+    phases ^= (1u << nch) - 1u;  // the chunk barriers this tile used
+    if (tid == 0) KMB_STAMP(3);
     // 5. store: C fragment (g, 2t + h) of each 8x8 tile -> (fiber j, row i)
 #pragma unroll
     for (int x = 0; x < 2; ++x)
@@ -233,11 +281,12 @@ __global__ void __launch_bounds__(THREADS) mumode_steps_kernel(const Params P) {
           const int i = r * BT + wn + y * 8 + 2 * t + h;
           dst[base + j * sa + static_cast<int64_t>(i) * sk] = make_double2(cr[x][y][h], ci[x][y][h]);
         }
-    __threadfence();
-    __syncthreads();  // every store of the tile (and every smem read) is done
+    __syncthreads();  // every store of the tile (and every shared-memory read) is done
 
-    // 6. publish: the consumer group this tile belongs to, and the product's total
+    // 6. publish (as a grid barrier does: CTA barrier, one fence, one release add): the
+    // consumer group this tile belongs to, and the product's total
     if (tid == 0) {
+      __threadfence();
       unsigned* c = P.cnt + static_cast<int64_t>(p) * CNT_STRIDE;
       int grp;
       if (mu == 0) grp = b * (n1 / BT) + r;            // (i3, i1-block) for dir 2
@@ -245,6 +294,7 @@ __global__ void __launch_bounds__(THREADS) mumode_steps_kernel(const Params P) {
       else grp = (b / BT) * (n3 / BT) + r;             // (i2-block, i3-block) for dir 1
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(c + grp) : "memory");
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(c + CNT_STRIDE - 1) : "memory");
+      KMB_STAMP(4);
     }
     ti += gridDim.x;
   }

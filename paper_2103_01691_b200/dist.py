@@ -50,14 +50,20 @@ class LocalStepper:
             None if self.post is None else ctypes.byref(self.post), stream))
         self.a, self.b = self.b, self.a
 
-    def run(self, steps):
-        """``steps`` exact steps.  A complex128 3D state whose extents are multiples of 32 up
-        to 96 (L2-resident: configuration 1) runs them as ONE persistent launch
-        (``km_steps_small``: the 3·steps sweeps as a dataflow of tiles, no per-product
-        launch, fill or partial wave); any other state steps one ``km_tucker`` at a time."""
+    def run(self, steps, persistent=False):
+        """``steps`` exact steps, one ``km_tucker`` launch each.
+
+        ``persistent=True`` runs them instead as ONE launch (``km_steps_small``: the 3·steps
+        sweeps as a dataflow of 32 x 32 tiles with dependency counters) for complex128 3D
+        states whose extents are multiples of 32 up to 96.  It is correct and kept for the
+        record, but measured slower than the per-step launches replayed as a CUDA graph
+        (64³ x 10 steps: 0.29-0.31 ms against 0.227 ms): a consumer tile of
+        the next sweep reads the output of ~all tiles of the previous one, so the sweeps
+        serialise on the tile latency (staging + MMA + publish), which exceeds a launch gap.
+        """
         if steps < 1:
             return
-        ws = self._steps_workspace(steps)
+        ws = self._steps_workspace(steps) if persistent else None
         if ws is None:
             for _ in range(steps):
                 self.step()

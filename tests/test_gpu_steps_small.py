@@ -35,7 +35,7 @@ def test_persistent_steps_match_oracle_and_step_loop(shape, steps):
     mats = cache.device_exps((np.complex128,) * 3, dev)
     st = dist.LocalStepper(dv.to_device(u, np.complex128, dev), mats)
     assert st._steps_workspace(steps) is not None
-    st.run(steps)
+    st.run(steps, persistent=True)
     got = dv.to_host(st.state)
     want = u
     for _ in range(steps):
@@ -51,7 +51,7 @@ def test_persistent_steps_match_oracle_and_step_loop(shape, steps):
     st2 = dist.LocalStepper(dv.to_device(u, np.complex128, dev), mats)
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        st2.run(steps)
+        st2.run(steps, persistent=True)
         torch.cuda.synchronize()
     names = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     assert sum("mumode_steps_kernel" in x for x in names) == 1, names
@@ -71,7 +71,7 @@ def test_repeated_runs_reuse_counters():
     mats = cache.device_exps((np.complex128,) * 3, dev)
     st = dist.LocalStepper(dv.to_device(u, np.complex128, dev), mats)
     for _ in range(5):
-        st.run(4)
+        st.run(4, persistent=True)
     want = u
     for _ in range(20):
         want = orc.step(cache.exps, want)
@@ -93,5 +93,5 @@ def test_ineligible_shapes_fall_back(shape):
     mats = [torch.from_numpy(np.ascontiguousarray(m)).to(dev) for m in mats_h]
     st = dist.LocalStepper(dv.to_device(u, np.complex128, dev), mats)
     assert st._steps_workspace(2) is None
-    st.run(2)
+    st.run(2, persistent=True)
     assert orc.rel_l2(dv.to_host(st.state), orc.step(mats_h, orc.step(mats_h, u))) <= 1e-12
