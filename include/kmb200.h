@@ -75,7 +75,23 @@ typedef struct km_pointop {
    * form the full product as inner[l] * w_d[i_d] (same rounding) without
    * per-element index divisions. */
   const double* inner_weights;
+  /* optional, any kind (KM_OP_NONE included): the two-norm of the values the
+   * product stores (after the op), accumulated in its epilogue instead of a
+   * separate pass over the result (reference: tensor.norm "two",
+   * tensor.py:169-198, as the GPE driver's drift, problems.py:596-599).  Every
+   * warp of every output tile writes one partial sum to a fixed slot of
+   * norm_ws (no atomics) and a one-warp kernel folds them in slot order into
+   * *norm_result = sqrt(sum |value|^2): deterministic.  norm_ws holds
+   * norm_ws_count doubles, at least km_norm_epilogue_slots().  Honoured by
+   * km_mumode, km_mumode_split and as km_tucker's post. */
+  double* norm_result;
+  double* norm_ws;
+  int64_t norm_ws_count;
 } km_pointop;
+
+/* doubles a km_pointop's norm_ws needs for a product with m rows and M fibers
+ * (M = n_left * n_right) */
+int64_t km_norm_epilogue_slots(int64_t m, int64_t fibers);
 
 /* kernel selection (process-wide, bit flags): AUTO picks the warp-specialised
  * TMA kernels where the shape allows and balances their last wave with

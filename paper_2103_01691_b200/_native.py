@@ -47,6 +47,7 @@ EXPORTS = (
     "km_stream_workspace_bytes",
     "km_steps_small_workspace_bytes",
     "km_steps_small",
+    "km_norm_epilogue_slots",
     "km_set_stream_workspace",
 )
 
@@ -64,6 +65,9 @@ class PointOp(ctypes.Structure):
         ("diag_dir", ctypes.c_int32),
         ("repeat", ctypes.c_int32),
         ("inner_weights", ctypes.c_void_p),
+        ("norm_result", ctypes.c_void_p),
+        ("norm_ws", ctypes.c_void_p),
+        ("norm_ws_count", ctypes.c_int64),
     ]
 
 
@@ -116,6 +120,8 @@ def _declare(lib):
     lib.km_set_kernel_policy.argtypes = [c_int]
     lib.km_steps_small_workspace_bytes.restype = c_int
     lib.km_steps_small_workspace_bytes.argtypes = [c_i64, c_i64, c_i64, c_i64, ctypes.POINTER(c_sz)]
+    lib.km_norm_epilogue_slots.restype = c_i64
+    lib.km_norm_epilogue_slots.argtypes = [c_i64, c_i64]
     lib.km_steps_small.restype = c_int
     lib.km_steps_small.argtypes = [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_sz, c_vp]
     lib.km_stream_workspace_bytes.restype = c_int

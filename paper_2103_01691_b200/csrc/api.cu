@@ -19,6 +19,9 @@ extern bool g_tc_halves_disabled;  // inst_tc32_c64.cu
 size_t tc32_workspace_bytes(int64_t m, int64_t K);  // inst_tc32_c64.cu
 size_t streamk_workspace_bytes();                    // inst_tma_c128.cu
 int bind_streamk_workspace(cudaStream_t st, void* ws, size_t bytes);  // inst_tma_c128.cu
+int norm_epilogue_finish(const km_pointop* op, bool fused, const void* out, int out_dt, int64_t n,
+                         cudaStream_t st);  // norm.cu
+int64_t norm_epilogue_slots(int64_t m, int64_t fibers);  // norm.cu
 int steps_small_workspace(int64_t n1, int64_t n2, int64_t n3, int64_t steps, size_t* bytes);  // inst_small.cu
 int launch_steps_small(void* state, const void* E1, const void* E2, const void* E3, int64_t n1, int64_t n2,
                        int64_t n3, int64_t steps, void* ws, size_t ws_bytes, cudaStream_t st);  // inst_small.cu
@@ -61,10 +64,13 @@ OpDev to_dev(const km_pointop* op) {
   int64_t in = 1;
   for (int i = 0; i + 1 < op->d; ++i) in *= op->dims[i];
   o.inner = in;
+  o.norm_ws = op->norm_result ? op->norm_ws : nullptr;
   return o;
 }
 
 int validate_op(const km_pointop* op, const char* where) {
+  if (op && op->norm_result && (!op->norm_ws || op->norm_ws_count < 1))
+    return fail(KM_EINVAL, "%s: epilogue norm without a partial-sum workspace", where);
   if (!op || op->kind == KM_OP_NONE) return KM_OK;
   if (op->d < 1 || op->d > KM_MAX_D) return fail(KM_EINVAL, "%s: op order %d outside 1..%d", where, op->d, KM_MAX_D);
   if (op->kind == KM_OP_GPE_PHASE) {
@@ -195,13 +201,19 @@ int mumode_impl(const void* u, int udt, const void* L, int ldt, void* out, int64
   const bool cu = is_complex(udt), cl = is_complex(ldt);
   auto launcher = is_double(udt) ? (cu ? (cl ? launch_d_cc : launch_d_cr) : (cl ? launch_d_rc : launch_d_rr))
                                  : (cu ? (cl ? launch_f_cc : launch_f_cr) : (cl ? launch_f_rc : launch_f_rr));
+  const bool want_norm = post && post->norm_result;
+  if (want_norm && post->norm_ws_count < norm_epilogue_slots(N, M))
+    return fail(KM_EINVAL, "km_mumode: epilogue norm workspace of %lld slots, %lld needed",
+                (long long)post->norm_ws_count, (long long)norm_epilogue_slots(N, M));
   int rc = launcher(u, L, out, M, N, K, nl, op, sp, st);
-  if (rc >= 0) return rc;
-  // op not fusable for this layout/dtype: plain product, then the op in place
+  if (rc >= 0) return rc ? rc : norm_epilogue_finish(post, true, out, promote(udt, ldt), M * N, st);
+  // op not fusable for this layout/dtype: plain product, then the op in place (and the norm
+  // as a separate pass)
   OpDev none;
   memset(&none, 0, sizeof(none));
   if ((rc = launcher(u, L, out, M, N, K, nl, none, sp, st))) return rc;
-  return pointwise_impl(out, out, promote(udt, ldt), M * N, post, st);
+  if ((rc = pointwise_impl(out, out, promote(udt, ldt), M * N, post, st))) return rc;
+  return norm_epilogue_finish(post, false, out, promote(udt, ldt), M * N, st);
 }
 
 // complex64 -> complex128, exact
@@ -448,8 +460,9 @@ int km_tucker(const void* u, int u_dtype, int d, const int64_t* dims, const void
   if ((rc = validate_op(pre, "km_tucker pre"))) return rc;
   if ((rc = validate_op(post, "km_tucker post"))) return rc;
   const bool has_pre = pre && pre->kind != KM_OP_NONE;
-  const bool has_post = post && post->kind != KM_OP_NONE;
-  if ((has_pre && !is_complex(u_dtype)) || (has_post && !is_complex(fdt)))
+  const bool has_post_op = post && post->kind != KM_OP_NONE;
+  const bool has_post = has_post_op || (post && post->norm_result);  // an op and/or the epilogue norm
+  if ((has_pre && !is_complex(u_dtype)) || (has_post_op && !is_complex(fdt)))
     return fail(KM_EINVAL, "km_tucker: pointwise ops need complex tensors");
 
   int active[KM_MAX_D];
@@ -466,8 +479,8 @@ int km_tucker(const void* u, int u_dtype, int d, const int64_t* dims, const void
       cudaError_t e = cudaMemcpyAsync(out, u, n_in * elem_bytes(u_dtype), cudaMemcpyDeviceToDevice, st);
       if (e != cudaSuccess) return fail(KM_ECUDA, "km_tucker copy: %s", cudaGetErrorString(e));
     }
-    if (has_post) return pointwise_impl(out, out, fdt, n_in, post, st);
-    return KM_OK;
+    if (has_post_op && (rc = pointwise_impl(out, out, fdt, n_in, post, st))) return rc;
+    return norm_epilogue_finish(post, false, out, fdt, n_in, st);
   }
   if ((na > 1 || has_pre) && !ws0) return fail(KM_EINVAL, "km_tucker: NULL workspace");
   if ((ws0 && (ws0 == u || ws0 == out)) || (ws1 && (ws1 == u || ws1 == out || ws1 == ws0)))

@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
     const int64_t f_q = KC ? 0 : m0 / nl;
     const int64_t f_rem = KC ? 0 : m0 - f_q * nl, f_slab = KC ? 0 : f_q * nl * sp.ncb;
     using TO = typename El<double, CU || CL>::T;
+    double nacc = 0.0;  // optional epilogue two-norm (op.norm_ws), this warp's share of the tile
     // visit the output addresses of one 8-row block of the warp tile: fn(dst, p, j, h, col)
     // for every in-range element of row i
     auto visit_row = [&](const int i, auto&& fn) {
@@ -449,6 +450,7 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
           if (with_op) apply_op_fast<OPK>(op, octx, lf, col, re, im);
         }
         dst[p] = narrow<TO>(re, im);
+        if (op.norm_ws) nacc = fma(re, re, fma(im, im, nacc));  // |stored value|^2 (f64 output)
       });
     };
     if constexpr (OPK == KM_OP_NONE) {
@@ -526,7 +528,9 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
             }
       }
     }
+    if (op.norm_ws) norm_slot(op.norm_ws, tile * CONSUMERS + warp, nacc);
   };
+  if (op.norm_ws) norm_count(op.norm_ws, tiles * CONSUMERS);
 
   if constexpr (!SKT) {
     for (int64_t tile = cta; tile < tiles; tile += S) run_tile(tile, 0, KT);

@@ -136,9 +136,51 @@ int norm_kind(const void* a, const void* b, int64_t n, int kind, const OpDev& w,
   return norm_t<T, 2>(a, b, n, w, out, ws, st);
 }
 
+// the epilogue two-norm's fold: slot count in ws[0] (written by the product), slots
+// ws[1..count] folded as norm_final_kernel does (fixed order: deterministic)
+__global__ void norm_epilogue_final_kernel(const double* __restrict__ ws, double* out) {
+  const long long np = *reinterpret_cast<const long long*>(ws);
+  double r = 0.0;
+  for (long long k = threadIdx.x; k < np; k += 32) r += ws[1 + k];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) r += __shfl_down_sync(0xffffffffu, r, off);
+  if (threadIdx.x == 0) out[0] = sqrt(r);
+}
+
+int64_t norm_epilogue_slots(int64_t m, int64_t fibers) {
+  // the finest tiling any product kernel uses: 16 x 16 tiles of four 8 x 8 warp tiles
+  const int64_t fine = ((fibers + 15) / 16) * ((m + 15) / 16) * 4;
+  const int64_t floor_ = norm_blocks() + 32;  // the separate-pass fallback's partials
+  return 1 + (fine > floor_ ? fine : floor_);
+}
+
+// after a product whose epilogue accumulated the norm (or, when the op was not fused,
+// a separate pass over `out`): *op->norm_result
+int norm_epilogue_finish(const km_pointop* op, bool fused, const void* out, int out_dt, int64_t n, cudaStream_t st) {
+  if (!op || !op->norm_result) return KM_OK;
+  if (op->norm_ws_count < norm_epilogue_slots(1, 1))
+    return fail(KM_EINVAL, "epilogue norm: workspace of %lld slots, %lld needed", (long long)op->norm_ws_count,
+                (long long)norm_epilogue_slots(1, 1));
+  if (fused) {
+    norm_epilogue_final_kernel<<<1, 32, 0, st>>>(op->norm_ws, op->norm_result);
+    return check_launch("norm_epilogue_final_kernel");
+  }
+  OpDev none;
+  memset(&none, 0, sizeof(none));
+  double* ws = op->norm_ws;
+  switch (out_dt) {
+    case KM_F32: return norm_t<float, 1>(out, nullptr, n, none, op->norm_result, ws, st);
+    case KM_F64: return norm_t<double, 1>(out, nullptr, n, none, op->norm_result, ws, st);
+    case KM_C64: return norm_t<float2, 1>(out, nullptr, n, none, op->norm_result, ws, st);
+    default: return norm_t<double2, 1>(out, nullptr, n, none, op->norm_result, ws, st);
+  }
+}
+
 }  // namespace kmb
 
 using namespace kmb;
+
+extern "C" int64_t km_norm_epilogue_slots(int64_t m, int64_t fibers) { return norm_epilogue_slots(m, fibers); }
 
 extern "C" size_t km_norm_workspace_bytes(void) { return static_cast<size_t>(norm_blocks()) * sizeof(double); }
 

@@ -86,6 +86,23 @@ def _diag_op(shape, factor_dev, direction):
     return op
 
 
+def _attach_norm(op, norm_out, dev, keep):
+    """Ask the product that applies ``op`` for the two-norm of what it stores (its epilogue's
+    per-warp partial sums, folded into ``norm_out[0]``); the partial-sum workspace is
+    sized for any product shape (km_norm_epilogue_slots of the largest) and kept alive."""
+    dims = [op.dims[i] for i in range(op.d)]
+    n = 1
+    for x in dims:
+        n *= x
+    # whichever direction's product ends up applying the op: (rows, fibers) = (n_mu, n / n_mu)
+    slots = max(_native.lib().km_norm_epilogue_slots(x, n // x) for x in dims)
+    ws = dv.torch.empty(int(slots), dtype=dv.torch.float64, device=dev)
+    keep.append(ws)
+    op.norm_result = norm_out.data_ptr()
+    op.norm_ws = ws.data_ptr()
+    op.norm_ws_count = int(slots)
+
+
 def _check_weights(weights, shape):
     # problems.py:528-539 messages
     if len(weights) != len(shape):
@@ -170,7 +187,7 @@ def gpe_strang_step(linear_cache, weights, psi, tau, _timer=None):
     return run()
 
 
-def gpe_strang_run(linear_cache, weights, psi, tau, steps):
+def gpe_strang_run(linear_cache, weights, psi, tau, steps, _norm_out=None):
     """``steps`` consecutive :func:`gpe_strang_step` calls (the loop of problems.py:597-598).
 
     Between two steps the closing half-phase of step k and the opening
@@ -178,6 +195,10 @@ def gpe_strang_run(linear_cache, weights, psi, tau, steps):
     last product (``repeat = 2``), so only the very first half-phase is a
     standalone pass.  Each rotation recomputes the density from the rotated
     value, so the result is bitwise that of the step-by-step loop.
+    
+    ``_norm_out`` (a one-element float64 device tensor, internal): the two-norm of the
+    final state, accumulated in the last product's epilogue (km_pointop.norm_result) -
+    the GPE driver's drift (problems.py:596-599) without another pass over the state.
     """
     po = _Operand(psi)
     if po.shape != linear_cache.shape:
@@ -203,9 +224,13 @@ def gpe_strang_run(linear_cache, weights, psi, tau, steps):
         state = po.obj if po.is_tensor and po.obj.is_cuda else dv.to_device(np.asarray(po.obj), out_dtype, dev)
         state = dv.tensor_as(state, out_dtype)
     mats = _cache_mats(linear_cache, _Operand(state))
+    last = single
+    if _norm_out is not None:
+        last = _gpe_op(po.shape, w_dev, half_tau, inner_dev, 1)
+        _attach_norm(last, _norm_out, dev, keep)
     for k in range(steps):
         pre = single if (k == 0 and not opened) else None
-        post = single if k == steps - 1 else double
+        post = last if k == steps - 1 else double
         state = run_tucker(state, mats, pre=pre, post=post, out_dtype=out_dtype, keepalive=keep)
     if po.is_tensor and po.obj.is_cuda:
         return state

@@ -16,7 +16,7 @@ HEADER = os.path.join(ROOT, "include", "kmb200.h")
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(km_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|size_t|const char\*)\s+(km_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_the_binding_exports():
@@ -41,8 +41,8 @@ def test_library_is_sm100a_cubin():
 
 
 def test_struct_layout_matches_header():
-    # km_pointop: 2*int32 + 8*int64 + 8*ptr + double + ptr + 2*int32 + ptr
-    assert ctypes.sizeof(_native.PointOp) == 8 + 64 + 64 + 8 + 8 + 8 + 8
+    # km_pointop: 2*int32 + 8*int64 + 8*ptr + double + ptr + 2*int32 + ptr + 2*ptr + int64
+    assert ctypes.sizeof(_native.PointOp) == 8 + 64 + 64 + 8 + 8 + 8 + 8 + 16 + 8
 
 
 def test_bad_dtype_rejected_without_device():
