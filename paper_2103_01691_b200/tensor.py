@@ -184,7 +184,9 @@ def run_tucker(u, mats, pre=None, post=None, out_dtype=None, keepalive=()):
     cdt = _compute_dtype(result)
     single = cdt in (np.dtype(np.float32), np.dtype(np.complex64))
     u_dt = _operand_dtype(uo.dtype, single)
-    if (pre is not None or post is not None) and u_dt.kind != "c":
+    # a phase op needs a complex state (a post carrying only the epilogue norm does not)
+    phased = any(op is not None and op.kind != _native.OP_NONE for op in (pre, post))
+    if phased and u_dt.kind != "c":
         u_dt = _operand_dtype(np.complex64, single)
 
     # the reference's per-product multiply-add tally (tensor.py:114-115)
