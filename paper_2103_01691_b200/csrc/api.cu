@@ -65,6 +65,7 @@ OpDev to_dev(const km_pointop* op) {
   for (int i = 0; i + 1 < op->d; ++i) in *= op->dims[i];
   o.inner = in;
   o.norm_ws = op->norm_result ? op->norm_ws : nullptr;
+  o.norm_count = op->norm_ws_count;
   return o;
 }
 
@@ -197,6 +198,17 @@ int mumode_impl(const void* u, int udt, const void* L, int ldt, void* out, int64
     sp = *split;
     if (!ksplit) sp.kbs = 0;
     if (!nsplit) sp.nbs = 0;
+  }
+  {  // logical extents (one past the largest index the layouts address), for KMB_CHECK builds
+    const int64_t nr_ = (M + nl - 1) / nl;  // M < nl: a fiber range of one slab (km_mumode_fibers)
+    const int64_t lmax = (M < nl ? M : nl) - 1;
+    auto extent = [&](int64_t len, int64_t blk, int64_t bstride) {
+      const int64_t j = len - 1;
+      const int64_t b = blk < len ? j / blk : 0, w = blk < len ? blk : len;
+      return b * (blk < len ? bstride : 0) + lmax + nl * (j - b * w) + nl * w * (nr_ - 1) + 1;
+    };
+    sp.in_ext = nl == 1 ? M * static_cast<int64_t>(K) : extent(K, sp.kcb, sp.kbs);
+    sp.out_ext = nl == 1 ? M * static_cast<int64_t>(N) : extent(N, sp.ncb, sp.nbs);
   }
   const bool cu = is_complex(udt), cl = is_complex(ldt);
   auto launcher = is_double(udt) ? (cu ? (cl ? launch_d_cc : launch_d_cr) : (cl ? launch_d_rc : launch_d_rr))

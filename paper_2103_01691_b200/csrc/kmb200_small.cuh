@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(THREADS) mumode_steps_kernel(const Params P) {
         KMB_STAMP(1);
       }
       __syncwarp();
+      KMB_ASSERT(base + (BT - 1) * sa + static_cast<int64_t>(K - 1) * sk < static_cast<int64_t>(n1) * n2 * n3);
       for (int c = 0; c < nch; ++c) {
         if (mu == 0) {
           bulk_g2s(As + lane * PK + c * BT, src + base + lane * sa + c * BT, BT * 16, &bars[c]);
@@ -279,6 +280,7 @@ __global__ void __launch_bounds__(THREADS) mumode_steps_kernel(const Params P) {
         for (int h = 0; h < 2; ++h) {
           const int j = wm + x * 8 + g;
           const int i = r * BT + wn + y * 8 + 2 * t + h;
+          KMB_ASSERT(base + j * sa + static_cast<int64_t>(i) * sk < static_cast<int64_t>(n1) * n2 * n3);
           dst[base + j * sa + static_cast<int64_t>(i) * sk] = make_double2(cr[x][y][h], ci[x][y][h]);
         }
     __syncthreads();  // every store of the tile (and every shared-memory read) is done

@@ -433,6 +433,7 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
     auto accum_row = [&](const int i, double (&crow)[4][2], double (&cirow)[4][2]) {
       visit_row(i, [&](TO* dst, int64_t p, int j, int h, int) {
         double re = crow[j][h], im = (CU || CL) ? cirow[j][h] : 0.0;
+        KMB_ASSERT(p >= 0 && p < sp.out_ext);
         add_old(dst[p], re, im);
         crow[j][h] = re;
         if constexpr (CU || CL) cirow[j][h] = im;
@@ -449,6 +450,7 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
         if constexpr (OPK != KM_OP_NONE && (CU || CL)) {
           if (with_op) apply_op_fast<OPK>(op, octx, lf, col, re, im);
         }
+        KMB_ASSERT(p >= 0 && (sp.peer[0] ? true : p < sp.out_ext));
         dst[p] = narrow<TO>(re, im);
         if (op.norm_ws) nacc = fma(re, re, fma(im, im, nacc));  // |stored value|^2 (f64 output)
       });
@@ -528,7 +530,7 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
             }
       }
     }
-    if (op.norm_ws) norm_slot(op.norm_ws, tile * CONSUMERS + warp, nacc);
+    if (op.norm_ws) norm_slot(op.norm_ws, tile * CONSUMERS + warp, nacc, op.norm_count);
   };
   if (op.norm_ws) norm_count(op.norm_ws, tiles * CONSUMERS);
 

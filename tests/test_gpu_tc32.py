@@ -82,3 +82,30 @@ def test_long_contractions(shape, mu, halves):
     e128, e64 = orc.rel_l2(got, want128), orc.rel_l2(got, want64)
     assert e128 <= (5e-6 if halves and kp <= 1024 else 2e-6), e128
     assert e64 <= 1e-5, e64
+
+
+@pytest.mark.parametrize("mu", [1, 2, 3])
+def test_complex64_state_with_real_float32_factor_on_tcgen05(mu):
+    """complex64 x float32 (the single-precision Hermite transforms): numpy promotes the real
+    factor to complex64 (tensor.py:121-123), so the product runs on the tcgen05 kernel with the
+    promoted factor; parity against the reference's own complex64 arithmetic."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    from paper_2103_01691_b200 import _device as dv
+
+    n = 128
+    rng = np.random.default_rng(mu)
+    u = np.asfortranarray((rng.standard_normal((n,) * 3) + 1j * rng.standard_normal((n,) * 3)).astype(np.complex64))
+    phi = (rng.standard_normal((n, n)) / np.sqrt(n)).astype(np.float32)
+    t = dv.to_device(u, np.complex64, torch.device("cuda", 0))
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        got = km.mu_mode_product(t, phi, mu)
+        torch.cuda.synchronize()
+    names = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    assert any("mumode_tc32" in x for x in names), names
+    got = dv.to_host(got)
+    assert got.dtype == np.complex64
+    want = orc.mu_mode_product(u, phi, mu)
+    assert orc.rel_l2(got, want) <= 1e-5
