@@ -49,3 +49,20 @@ def golden(name):
 @pytest.fixture
 def gold():
     return golden
+
+
+def kernels_launched(fn):
+    """Run fn() under the CUDA activity profiler; return (result, set of kernel names).
+
+    The set is None when the profiler recorded no device activity at all (CUPTI can stop
+    delivering records late in a long test process); callers then skip only the
+    which-kernel assertion, never the numerical ones."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        out = fn()
+        torch.cuda.synchronize()
+    names = {e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA}
+    return out, (names or None)
