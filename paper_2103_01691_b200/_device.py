@@ -129,6 +129,16 @@ def _bind_stream_workspace(idx, raw):
     _BOUND[(idx, raw)] = ws
 
 
+def on_device(dev):
+    """Context making ``dev`` (a CUDA torch.device, or None) the current device when it is not
+    already; the library's set-up caches and launches follow the current device."""
+    import contextlib
+
+    if dev is None or dev.index is None or dev.index == torch.cuda.current_device():
+        return contextlib.nullcontext()
+    return torch.cuda.device(dev)
+
+
 def is_fortran(t):
     """Column-major dense (size-1 extents may carry any stride)."""
     s = 1

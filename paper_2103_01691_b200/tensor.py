@@ -168,6 +168,14 @@ def launch_product(src_ptr, src_code, mat_ptr, mat_code, dst_ptr, m, nl, nmu, nr
 
 
 def run_tucker(u, mats, pre=None, post=None, out_dtype=None, keepalive=()):
+    """:func:`_run_tucker` with the tensor's device current (the C ABI launches on the current
+    device: a CUDA tensor on another GPU than the current one is handled there)."""
+    uo = u.device if dv.is_tensor(u) and u.is_cuda else None
+    with dv.on_device(uo):
+        return _run_tucker(u, mats, pre, post, out_dtype, keepalive)
+
+
+def _run_tucker(u, mats, pre=None, post=None, out_dtype=None, keepalive=()):
     """Core device driver: ``post(pre(u) x_1 mats[0] ... x_d mats[d-1])``.
 
     ``u``/``mats`` are already validated.  ``pre``/``post`` are
@@ -386,6 +394,11 @@ _NORM_WS = {}
 
 def device_norm(a, kind, weights=None, b=None):
     """||a - b|| (b optional) through the ``km_norm`` kernels; ``a``/``b`` numpy or CUDA tensors."""
+    with dv.on_device(a.device if dv.is_tensor(a) and a.is_cuda else None):
+        return _device_norm(a, kind, weights, b)
+
+
+def _device_norm(a, kind, weights=None, b=None):
     ao = _Operand(a)
     dev = ao.obj.device if ao.is_tensor and ao.obj.is_cuda else dv.device()
     dt = _compute_dtype(np.result_type(ao.dtype, *([] if b is None else [_Operand(b).dtype])))
