@@ -175,6 +175,112 @@ def run_tucker(u, mats, pre=None, post=None, out_dtype=None, keepalive=()):
         return _run_tucker(u, mats, pre, post, out_dtype, keepalive)
 
 
+_TORCH_SAME_PRECISION = {}
+if dv.torch is not None:
+    _t = dv.torch
+    for _u in (_t.float64, _t.complex128):
+        for _m in (_t.float64, _t.complex128):
+            _TORCH_SAME_PRECISION[(_u, _m)] = _m
+    for _u in (_t.float32, _t.complex64):
+        for _m in (_t.float32, _t.complex64):
+            _TORCH_SAME_PRECISION[(_u, _m)] = _m
+
+_PLANS = {}
+_PLANS_MAX = 256
+
+
+def _fast_tucker(u, mats, pre, post, out_dtype, keepalive):
+    """The device-resident case of :func:`_run_tucker` from a per-shape plan.
+
+    A column-major CUDA tensor with device-tensor factors of its own precision (e.g. a
+    PropagatorCache's device copies) needs none of the dtype walks, workspace queries and
+    ctypes array builds per call: they are memoised per (shapes, dtypes, op presence,
+    device).  Returns None when the plan does not apply (the general path then runs).
+    """
+    if not dv.is_fortran(u) or len(mats) > _native.MAX_D or \
+            not all(m is None or dv.is_tensor(m) for m in mats):
+        return None
+    key = (tuple(u.shape), u.dtype, u.device, out_dtype,
+           tuple(None if m is None else (tuple(m.shape), m.dtype, m.device, m.is_contiguous()) for m in mats),
+           pre is None, post is None, None if pre is None else pre.kind, None if post is None else post.kind)
+    plan = _PLANS.get(key)
+    if plan is None:
+        if any(m is not None and (not dv.is_tensor(m) or m.device != u.device or not m.is_contiguous()
+                                  or m.dtype != _TORCH_SAME_PRECISION.get((u.dtype, m.dtype), None))
+               for m in mats):
+            _PLANS[key] = False
+            return None
+        plan = _make_plan(u, mats, pre, post, out_dtype)
+        if len(_PLANS) >= _PLANS_MAX:
+            _PLANS.pop(next(iter(_PLANS)))
+        _PLANS[key] = plan
+    if plan is False:
+        return None
+    (d, out_shape, cdt_t, u_code, c_dims, c_codes, c_rows, need, fits, nact, macs, finish_dt) = plan
+    for mac in macs:
+        _tally(mac)
+    dev = u.device
+    lib = _native.lib()
+    out = dv.fortran_empty(out_shape, cdt_t, dev)
+    c_mats = (ctypes.c_void_p * d)(*[None if m is None else m.data_ptr() for m in mats])
+    ws0 = dv.torch.empty(max(need, 1), dtype=dv.torch.uint8, device=dev) if need else None
+    ws1 = dv.torch.empty(max(need, 1), dtype=dv.torch.uint8, device=dev) if need and nact > 1 and not fits else None
+    _native.check(lib.km_tucker(
+        u.data_ptr(), u_code, d, c_dims, c_mats, c_codes, c_rows, out.data_ptr(),
+        None if ws0 is None else ws0.data_ptr(), None if ws1 is None else ws1.data_ptr(),
+        None if pre is None else ctypes.byref(pre), None if post is None else ctypes.byref(post),
+        dv.stream_ptr(dev)))
+    del ws0, ws1, keepalive
+    if finish_dt is not None:
+        out = dv.tensor_as(out, finish_dt)
+    return out
+
+
+def _make_plan(u, mats, pre, post, out_dtype):
+    d = u.dim()
+    udt = dv.np_dtype(u.dtype)
+    result = np.result_type(udt, *[dv.np_dtype(m.dtype) for m in mats if m is not None])
+    if out_dtype is not None:
+        result = np.result_type(result, out_dtype)
+    cdt = _compute_dtype(result)
+    phased = any(op is not None and op.kind != _native.OP_NONE for op in (pre, post))
+    if phased and udt.kind != "c":
+        return False
+    if udt == np.dtype(np.complex64) and any(m is not None and not m.is_complex() for m in mats):
+        return False  # complex64 x real float32: the general path promotes the factor (tcgen05)
+    cur, macs, codes, rows = list(u.shape), [], [], []
+    for mu, m in enumerate(mats):
+        if m is None:
+            codes.append(0)
+            rows.append(0)
+            continue
+        macs.append(m.shape[0] * prod(cur))
+        cur[mu] = m.shape[0]
+        codes.append(dv.code(dv.np_dtype(m.dtype)))
+        rows.append(m.shape[0])
+    out_shape = tuple(cur)
+    if any(n == 0 for n in u.shape) or any(n == 0 for n in out_shape):
+        return False
+    if udt == np.dtype(np.complex64) and pre is None and post is None and \
+            all(c == _native.KM_C64 for m, c in zip(mats, codes) if m is not None):
+        return False  # the tcgen05 loop (per-product launches) of the general path
+    c_dims = (ctypes.c_int64 * d)(*u.shape)
+    c_codes = (ctypes.c_int * d)(*codes)
+    c_rows = (ctypes.c_int64 * d)(*rows)
+    c_probe = (ctypes.c_void_p * d)(*[None if m is None else 1 for m in mats])
+    ws = ctypes.c_size_t(0)
+    u_code = dv.code(udt)
+    _native.check(_native.lib().km_tucker_workspace(u_code, d, c_dims, c_probe, c_codes, c_rows, ctypes.byref(ws)))
+    nact = sum(m is not None for m in mats)
+    need = ws.value if (nact > 1 or pre is not None) else 0
+    out_bytes = prod(out_shape) * cdt.itemsize
+    fits = need <= out_bytes
+    finish_dt = result if result != cdt and result in dv.SUPPORTED else None
+    if result != cdt and result not in dv.SUPPORTED:
+        return False
+    return (d, out_shape, dv.torch_dtype(cdt), u_code, c_dims, c_codes, c_rows, need, fits, nact, macs, finish_dt)
+
+
 def _run_tucker(u, mats, pre=None, post=None, out_dtype=None, keepalive=()):
     """Core device driver: ``post(pre(u) x_1 mats[0] ... x_d mats[d-1])``.
 
@@ -183,6 +289,10 @@ def _run_tucker(u, mats, pre=None, post=None, out_dtype=None, keepalive=()):
     (used by the splitting schemes).  Returns numpy for numpy input and a
     device tensor for tensor input.
     """
+    if dv.is_tensor(u) and u.is_cuda:
+        res = _fast_tucker(u, mats, pre, post, out_dtype, keepalive)
+        if res is not None:
+            return res
     uo = _Operand(u)
     mos = [None if m is None else _Operand(m) for m in mats]
     d = uo.ndim
