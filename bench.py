@@ -394,11 +394,15 @@ def run_ours(args):
             "clocks": clocks.summary(),
             "gpu_launches": runner.launches_per_step * args.steps,
         }
-        print(json.dumps(line), flush=True)
     if slab:
         import torch.distributed as tdist
 
+        # every rank is done before the communicators go (their teardown lines come first),
+        # so rank 0's JSON line is the last thing it prints
+        tdist.barrier()
         tdist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
 
 
 def launch_ranks(args, argv):
