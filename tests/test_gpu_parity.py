@@ -516,3 +516,22 @@ def test_matvec_accumulates_like_the_reference(dtype, tol):
     for mu in (2, 3):
         ref += orc.mu_mode_product(u, facs[mu - 1], mu)
     assert rel(got, ref) <= (1e-12 if tol == 0.0 else tol)
+
+
+@pytest.mark.parametrize("shape,dtype", [((33, 17, 5), np.complex128), ((7, 40, 9), np.float64),
+                                         ((19, 3, 31), np.complex64), ((65, 1, 2), np.complex128),
+                                         ((256, 256, 256), np.complex128)])
+def test_matvec_ragged_and_full_size(shape, dtype):
+    """The accumulating epilogue on ragged tiles (edge rows / fibers), a size-1 direction, and
+    the 256^3 TMA kernel, against the reference's out += p (kron.py:94-102) on the oracle."""
+    rng = np.random.default_rng(sum(shape))
+    cplx = np.dtype(dtype).kind == "c"
+    u = crand(rng, shape, dtype) if cplx else np.asfortranarray(rng.standard_normal(shape).astype(dtype))
+    facs = tuple(((rng.standard_normal((n, n)) + (1j * rng.standard_normal((n, n)) if cplx else 0)) / np.sqrt(n))
+                 .astype(dtype) for n in shape)
+    got = km.matvec(km.KroneckerOp(facs), u)
+    want = orc.mu_mode_product(u, facs[0], 1)
+    for mu in range(2, 4):
+        want = want + orc.mu_mode_product(u, facs[mu - 1], mu)
+    assert got.dtype == want.dtype and got.shape == want.shape
+    assert rel(got, want) <= TOL[np.dtype(dtype)]

@@ -167,3 +167,44 @@ def test_stream_workspace_entry_points():
     assert rc == _native.KM_EINVAL and b"needed" in lib.km_last_error()
     # unbinding a stream that has no workspace is a no-op
     assert lib.km_set_stream_workspace(None, None, 0) == 0
+
+
+def test_round2_entry_points_reject_bad_arguments_before_launch():
+    lib = _native.lib()
+    p = ctypes.c_void_p(0x1000)
+    # accumulate must be 0 or 1
+    rc = lib.km_mumode_split(p, _native.KM_C128, p, _native.KM_C128, p, 16, 4, 16, 2, 16, 0, 16, 0, 2, None, None)
+    assert rc == _native.KM_EINVAL and b"accumulate" in lib.km_last_error()
+    # widening pointwise: complex128 -> complex64 would round; widening in place is impossible
+    assert lib.km_pointwise_cast(p, _native.KM_C128, ctypes.c_void_p(0x2000), _native.KM_C64, 8, None, None) \
+        == _native.KM_EINVAL
+    assert lib.km_pointwise_cast(p, _native.KM_C64, p, _native.KM_C128, 8, None, None) == _native.KM_EINVAL
+    assert lib.km_pointwise_cast(p, _native.KM_F64, p, _native.KM_F64, 8, None, None) == _native.KM_EINVAL
+    # the steps kernel's shape rules: multiples of 32 in [32, 96], steps >= 1
+    nb = ctypes.c_size_t()
+    for shape, steps in (((48, 64, 64), 1), ((128, 64, 64), 1), ((64, 64, 16), 1), ((64, 64, 64), 0)):
+        assert lib.km_steps_small_workspace_bytes(*shape, steps, ctypes.byref(nb)) == _native.KM_EINVAL
+    assert lib.km_steps_small_workspace_bytes(64, 64, 64, 10, ctypes.byref(nb)) == 0
+    assert nb.value >= 2 * 64**3 * 16 + 30 * 512 * 4
+    # a too-small steps workspace, and a misaligned stream-K workspace
+    assert lib.km_steps_small(p, p, p, p, 64, 64, 64, 10, p, 16, None) == _native.KM_EINVAL
+    big = ctypes.c_size_t()
+    assert lib.km_stream_workspace_bytes(ctypes.byref(big)) == 0
+    assert lib.km_set_stream_workspace(None, ctypes.c_void_p(0x1008), big.value) == _native.KM_EINVAL
+
+
+def test_epilogue_norm_contract_checked():
+    lib = _native.lib()
+    p = ctypes.c_void_p(0x1000)
+    op = _native.PointOp()
+    op.kind = _native.OP_NONE
+    op.d = 3
+    op.norm_result = 0x3000  # a result without a partial-sum workspace
+    rc = lib.km_mumode(p, _native.KM_C128, p, _native.KM_C128, p, 16, 1, 16, 16, ctypes.byref(op), None)
+    assert rc == _native.KM_EINVAL and b"norm" in lib.km_last_error()
+    op.norm_ws = 0x4000
+    op.norm_ws_count = 4  # too few slots for this product
+    rc = lib.km_mumode(p, _native.KM_C128, p, _native.KM_C128, p, 16, 1, 16, 16, ctypes.byref(op), None)
+    assert rc == _native.KM_EINVAL and b"slots" in lib.km_last_error()
+    # enough for any tiling of m = 256 rows x 65536 fibers
+    assert lib.km_norm_epilogue_slots(256, 65536) >= (65536 // 16) * (256 // 16) * 4
