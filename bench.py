@@ -144,6 +144,20 @@ def traffic_from_profile():
         return None
 
 
+def cpu_model():
+    """The host CPU's model name (lscpu's "Model name", from /proc/cpuinfo)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
 def cpu_reference(u, cache, budget_s, max_steps):
     """The reference algorithm (oracle numpy restatement) on all host threads."""
     from threadpoolctl import threadpool_info, threadpool_limits
@@ -168,6 +182,7 @@ def cpu_reference(u, cache, budget_s, max_steps):
         "value": sps,
         "unit": "steps/s",
         "cores": cores,
+        "cpu_model": cpu_model(),
         "kind": "port",
         "sample": f"{len(times)} full 256^3 c128 steps after 1 warm-up, numpy.matmul ({'; '.join(blas)})",
         "gflops": sps * FLOP_PER_STEP / 1e9,

@@ -302,7 +302,18 @@ def main():
     ap.add_argument("--only", default="12345ms")
     args = ap.parse_args()
     cores = os.cpu_count() or 1
-    res = {"cores": cores, "configs": []}
+    from threadpoolctl import threadpool_info
+
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), model)
+    except OSError:
+        pass
+    res = {"cores": cores, "cpu_model": model,
+           "blas": [f"{i.get('internal_api')} {i.get('version')} x{i.get('num_threads')}" for i in threadpool_info()],
+           "configs": []}
+    print(json.dumps({"cores": cores, "cpu_model": model, "blas": res["blas"]}), flush=True)
     fns = {"1": config1, "2": config2, "3": config3, "4": config4, "5": config5, "m": config_magnus, "s": config_c64}
     with threadpool_limits(limits=cores):
         for key in args.only:
