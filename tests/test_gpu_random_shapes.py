@@ -45,7 +45,7 @@ def _case(seed):
 def test_random_mu_mode_product(seed):
     rng, shape, mu, m, udt, ldt = _case(seed)
     u = _rand(rng, shape, udt)
-    mat = _rand(rng, (m, shape[mu - 1]), ldt) / np.sqrt(shape[mu - 1])
+    mat = (_rand(rng, (m, shape[mu - 1]), ldt) / np.sqrt(shape[mu - 1])).astype(ldt)  # keep the factor's dtype
     got = km.mu_mode_product(u, mat, mu)
     want = orc.mu_mode_product(u, mat, mu)
     assert got.shape == want.shape and got.dtype == want.dtype
@@ -60,7 +60,7 @@ def test_random_accumulate_into_output(seed):
     rng, shape, mu, m, udt, ldt = _case(seed)
     cdt = np.result_type(udt, ldt)
     u = _rand(rng, shape, udt)
-    mat = _rand(rng, (m, shape[mu - 1]), ldt) / np.sqrt(shape[mu - 1])
+    mat = (_rand(rng, (m, shape[mu - 1]), ldt) / np.sqrt(shape[mu - 1])).astype(ldt)
     out_shape = shape[:mu - 1] + (m,) + shape[mu:]
     out0 = _rand(rng, out_shape, cdt)
     dev = torch.device("cuda", 0)
