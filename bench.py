@@ -262,6 +262,96 @@ def e2e_slabs(runner, u_host, rank, world, dev, args):
             "call": "dist.SlabStepper: per-rank pinned slab -> device, one distributed step, slab -> pinned host"}
 
 
+def config_sweep(dev):
+    """Every BASELINE.json configuration on this GPU, device-resident: ms per unit, TFLOP/s at the
+    8-flop-per-complex-MAC convention (4 for real x complex, 2 for real x real) and the fraction of
+    the measured DMMA peak.  Parity of each one at its BASELINE size is the -m gpu tests'
+    (tests/test_gpu_configs.py); the CPU reference times are tools/bench_configs.py's."""
+    import torch
+
+    import paper_2103_01691_b200 as km
+    from paper_2103_01691_b200 import _device as dv
+    from paper_2103_01691_b200 import dist
+    from paper_2103_01691_b200.hermite import physical_propagator
+    from paper_2103_01691_b200.problems import schrodinger_initial_state, ti_potentials, weighted_vortex_state
+
+    peak, _ = fp64_peak()
+
+    def dev_ms(fn, reps, warm=3):
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    def entry(name, ms, flop, unit):
+        tf = flop / (ms * 1e-3) / 1e12
+        return {"config": name, "ms": ms, "unit": unit, "tflops": tf, "frac_of_dmma_peak": tf / peak}
+
+    rng = np.random.default_rng(0)
+    out = []
+    # 1: 64^3 c128, 10 exact steps, per-step launches in a CUDA graph
+    n = 64
+    d2 = km.heat_factors(n, 2).factors[0]
+    c1 = km.prepare(km.KroneckerOp((1j * d2,) * 3), 0.01)
+    u1 = np.asfortranarray(rng.standard_normal((n,) * 3) + 1j * rng.standard_normal((n,) * 3))
+    st = dist.LocalStepper(dv.to_device(u1, np.complex128, dev), c1.device_exps((np.complex128,) * 3, dev))
+    for _ in range(3):
+        st.step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(10):
+                st.step()
+    torch.cuda.synchronize()
+    out.append(entry("1: Schrodinger free 64^3 c128, 10 steps (CUDA graph)", dev_ms(g.replay, 50), 10 * 8 * 3 * n**4,
+                     "ms per 10 steps"))
+    del g, st
+    # 2: pipe flow 1024^2 f64, one exact step
+    n = 1024
+    c2 = km.prepare(km.pipeflow_factors(n), 4.0 / 8)
+    rho, z = np.linspace(0.1, 5.0, n), np.linspace(0.0, 8.0, n)
+    u2 = np.asfortranarray(np.exp(-8.0 * (rho - 2.55) ** 2)[:, None] * np.exp(-8.0 * (z - 1.5) ** 2)[None, :])
+    st = dist.LocalStepper(dv.to_device(u2, np.float64, dev), c2.device_exps((np.float64,) * 2, dev))
+    out.append(entry("2: pipe flow 1024^2 f64, one step", dev_ms(st.step, 50), 2 * 2 * n**3, "ms per step"))
+    del st
+    # 3: HKP 256^3: forward transform + exact step + inverse transform
+    k = 256
+    b = km.hermite_basis(k)
+    op = km.KroneckerOp(tuple(km.hamiltonian_factor(b, v) for v in ti_potentials()))
+    c3 = km.prepare(op, 1.0)
+    p3 = dv.to_device(schrodinger_initial_state((b.nodes,) * 3), np.complex128, dev)
+    hkp = lambda: km.inverse_transform((b,) * 3, km.step(c3, km.forward_transform((b,) * 3, p3)))  # noqa: E731
+    out.append(entry("3: HKP 256^3 c128 forward + step + inverse", dev_ms(hkp, 10), 4 * 3 * k**4 * 2 + 8 * 3 * k**4,
+                     "ms per solve"))
+    # 4: TD-potential Strang step 256^3 (E3 folded per step)
+    tau = 0.02
+    pp = physical_propagator(b, tau)
+    c4 = km.PropagatorCache(tau, (pp, pp, pp))
+    out.append(entry("4: TD-potential Strang 256^3 c128, one step",
+                     dev_ms(lambda: km.tdpot_strang_step(c4, b.nodes, p3, 0.3, tau), 10), 8 * 3 * k**4, "ms per step"))
+    del p3
+    torch.cuda.empty_cache()
+    # 5: GPE Strang step 512^3 c128 (and per step of a fused run)
+    n = 512
+    grids, lin_op, weights = km.gpe_setup(n)
+    c5 = km.prepare(lin_op, 0.1)
+    p5 = dv.to_device(weighted_vortex_state(grids, weights), np.complex128, dev)
+    out.append(entry("5: GPE Strang 512^3 c128, one step", dev_ms(lambda: km.gpe_strang_step(c5, weights, p5, 0.1), 3,
+                                                                   warm=1), 8 * 3 * n**4, "ms per step"))
+    del p5
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
 
@@ -409,6 +499,11 @@ def run_ours(args):
             "clocks": clocks.summary(),
             "gpu_launches": runner.launches_per_step * args.steps,
         }
+        if not slab and not args.no_configs:
+            try:
+                line["configs"] = config_sweep(dev)
+            except Exception as exc:  # the sweep must not lose the headline line
+                line["configs"] = {"error": f"{type(exc).__name__}: {exc}"}
     if slab:
         import torch.distributed as tdist
 
@@ -467,6 +562,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE config sweep (N = 1)")
     ap.add_argument("--slab", action="store_true", help="run the multi-GPU slab path even on one rank (testing)")
     ap.add_argument("--exchange", choices=["nccl", "peer"], default="nccl",
                     help="multi-GPU all-to-all: NCCL, or fused into the products via NVLink peer stores")
