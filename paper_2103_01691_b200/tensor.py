@@ -236,6 +236,56 @@ def _fast_tucker(u, mats, pre, post, out_dtype, keepalive):
     return out
 
 
+class StepPlan:
+    """A fully prebuilt ``km_tucker`` call for fixed device factors (a PropagatorCache's):
+    ctypes arrays, workspace size, output shape and dtype, and one reusable scratch buffer per
+    stream (calls on one stream are ordered, so consecutive steps may share it).  The hot
+    loop of small states calls ``run`` and nothing else (kron.step's fast path)."""
+
+    __slots__ = ("mats", "plan", "c_mats", "ws", "dev")
+
+    def __init__(self, u, mats):
+        self.mats = tuple(mats)
+        same = all(m is None or (dv.is_tensor(m) and m.device == u.device and m.is_contiguous()
+                                 and m.dtype == _TORCH_SAME_PRECISION.get((u.dtype, m.dtype)))
+                   for m in self.mats)
+        self.plan = _make_plan(u, self.mats, None, None, None) if same else False
+        self.dev = u.device
+        if self.plan is not False:
+            d = self.plan[0]
+            self.c_mats = (ctypes.c_void_p * d)(*[None if m is None else m.data_ptr() for m in self.mats])
+        self.ws = {}
+
+    @property
+    def ok(self):
+        return self.plan is not False
+
+    def run(self, u):
+        (d, out_shape, cdt_t, u_code, c_dims, c_codes, c_rows, need, fits, nact, macs, finish_dt) = self.plan
+        for mac in macs:
+            _tally(mac)
+        dev = self.dev
+        stream = dv.stream_ptr(dev)
+        out = dv.fortran_empty(out_shape, cdt_t, dev)
+        ws0 = ws1 = None
+        if need:
+            bufs = self.ws.get(stream.value)
+            if bufs is None:
+                n1 = 2 if (nact > 1 and not fits) else 1
+                bufs = [dv.torch.empty(max(need, 1), dtype=dv.torch.uint8, device=dev) for _ in range(n1)]
+                if len(self.ws) >= 4:
+                    self.ws.pop(next(iter(self.ws)))
+                self.ws[stream.value] = bufs
+            ws0 = bufs[0]
+            ws1 = bufs[1] if len(bufs) > 1 else None
+        _native.check(_native.lib().km_tucker(
+            u.data_ptr(), u_code, d, c_dims, self.c_mats, c_codes, c_rows, out.data_ptr(),
+            None if ws0 is None else ws0.data_ptr(), None if ws1 is None else ws1.data_ptr(), None, None, stream))
+        if finish_dt is not None:
+            out = dv.tensor_as(out, finish_dt)
+        return out
+
+
 def _make_plan(u, mats, pre, post, out_dtype):
     d = u.dim()
     udt = dv.np_dtype(u.dtype)
