@@ -47,3 +47,40 @@ def test_cache_hit_returns_the_same_device_copy():
     # same buffer, another target dtype: a separate entry
     t4 = dv.cached_vector(a, np.float32, dev)
     assert t4.dtype == torch.float32 and float(t4[0, 0]) == -1.0
+
+
+def test_step_plan_reuse_across_streams_and_dtypes():
+    """kron.step's prebuilt call (StepPlan): correct on repeated calls, on a second stream (its own
+    scratch buffer), for a float32 state with complex128 factors (no plan: the general path
+    promotes), and the flop tally still counts every product."""
+    import numpy as np
+    import torch
+
+    import paper_2103_01691_b200 as km
+    from oracle import kronmode_oracle as orc
+    from paper_2103_01691_b200 import _device as dv
+
+    dev = torch.device("cuda", 0)
+    n = 24
+    rng = np.random.default_rng(12)
+    u = np.asfortranarray(rng.standard_normal((n,) * 3) + 1j * rng.standard_normal((n,) * 3))
+    d2 = km.heat_factors(n, 2).factors[0]
+    cache = km.prepare(km.KroneckerOp((1j * d2,) * 3), 0.01)
+    t = dv.to_device(u, np.complex128, dev)
+    with km.count_flops() as fc:
+        a = km.step(cache, t)
+        b = km.step(cache, a)
+    assert fc.macs == 2 * 3 * n**4
+    want1 = orc.step(cache.exps, u)
+    want2 = orc.step(cache.exps, want1)
+    assert orc.rel_l2(dv.to_host(a), want1) <= 1e-12 and orc.rel_l2(dv.to_host(b), want2) <= 1e-12
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        c = km.step(cache, t)
+        d = km.step(cache, c)
+    s.synchronize()
+    assert np.array_equal(dv.to_host(c), dv.to_host(a)) and np.array_equal(dv.to_host(d), dv.to_host(b))
+    t32 = dv.to_device(u.real.astype(np.float32), np.float32, dev)
+    r = km.step(cache, t32)
+    assert dv.np_dtype(r.dtype) == np.complex128
+    assert orc.rel_l2(dv.to_host(r), orc.step(cache.exps, u.real.astype(np.float32))) <= 1e-12
