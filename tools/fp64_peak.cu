@@ -48,6 +48,62 @@ __global__ void dfma_loop(double* out, int iters, double seed) {
   if (s == 12345.678) out[threadIdx.x] = s;
 }
 
+// half the warps of each CTA run DMMA chains, the other half DFMA chains: does the FP64
+// datapath serve both at once (sum of the two rates) or share one pipe?
+__global__ void mixed_loop(double* out, int iters, double seed) {
+  const int warp = threadIdx.x >> 5;
+  double a = seed + threadIdx.x * 1e-9, b = seed * 0.5;
+  double acc[8][2];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) { acc[c][0] = 0.0; acc[c][1] = c * 1e-12; }
+  if (warp % 2 == 0) {
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(acc[c][0]), "+d"(acc[c][1]) : "d"(a), "d"(b));
+    }
+  } else {
+    for (int it = 0; it < iters * 4; ++it) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c][0] = fma(a, b, acc[c][0]);
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += acc[c][0] + acc[c][1];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+static int run_mixed(int warps) {
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  double* out;
+  CK(cudaMalloc(&out, 4096 * sizeof(double)));
+  const int iters = 20000;
+  dim3 grid(sms), block(32 * warps);
+  mixed_loop<<<grid, block>>>(out, iters, 1.0);
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0);
+    mixed_loop<<<grid, block>>>(out, iters, 1.0);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  // per SM: warps/2 DMMA warps x iters x 8 chains x 512 flop; warps/2 DFMA warps x 4 iters x 8 x 64 flop
+  const double dmma = double(sms) * (warps / 2) * iters * 8 * 512.0;
+  const double dfma = double(sms) * (warps / 2) * iters * 4.0 * 8 * 64.0;
+  printf("mixed DMMA + DFMA warps/SM=%3d  %.3f ms  DMMA part %.2f + DFMA part %.2f = %.2f TFLOP/s\n", warps, best,
+         dmma / (best * 1e-3) / 1e12, dfma / (best * 1e-3) / 1e12, (dmma + dfma) / (best * 1e-3) / 1e12);
+  cudaFree(out);
+  return 0;
+}
+
 template <typename K>
 static int run(const char* name, K kern, int warps_per_cta, int ctas_per_sm, int iters, double flop_per_thread_iter) {
   int sms = 0;
@@ -113,5 +169,6 @@ int main(int argc, char** argv) {
   run("dmma m8n8k4 chains=16", dmma_loop<16>, 8, 1, iters / 2, 16 * 16.0);
   run("dmma m8n8k4 chains=2", dmma_loop<2>, 16, 1, iters * 4, 2 * 16.0);
   for (int w : {8, 16, 32}) run("dfma chains=8", dfma_loop<8>, w, 1, iters * 4, 8 * 2.0);
+  for (int w : {8, 16}) run_mixed(w);
   return 0;
 }
