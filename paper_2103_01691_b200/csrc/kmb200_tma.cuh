@@ -9,9 +9,12 @@
 //   * all eight warps wait on "full", run their 4x4-tile DMMA.8x8x4 warp tiles
 //     straight out of the swizzled stage, and release the stage with one
 //     arrive per warp on its "empty" mbarrier — no __syncthreads in the loop.
-//     (A dedicated producer warp would put a third warp on one SM
-//     sub-partition and cap every thread at 168 registers; the accumulators
-//     alone need 128.)
+//     (A dedicated producer warp puts a third warp on one SM sub-partition
+//     and caps every thread at 168 registers; the complex accumulators alone
+//     need 128, so only the real x real products, 64 accumulator registers,
+//     use one: there it walks the whole ring and takes the load bookkeeping
+//     off warp 0, which otherwise paces the CTA — 3.4 % on a 512^3 f64
+//     product, tools/ab_probe.py.)
 //   * the grid is persistent (one CTA per SM) and walks the tiles with a
 //     static stride; the k-block counter runs across tiles, so the loads of
 //     tile i+1 are in flight during the epilogue of tile i.
@@ -51,6 +54,20 @@ constexpr int THREADS = 32 * CONSUMERS;
 constexpr int AHEAD = KMB_TMA_AHEAD;  // k-blocks between a stage's load and its use
 constexpr int A_BYTES = BM * BKS * 16, B_BYTES = BN * BKS * 16, STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int SMEM_BYTES = TSTAGES * STAGE_BYTES + 2 * TSTAGES * 8 + 1024;
+#ifndef KMB_TMA_SW64
+#define KMB_TMA_SW64 1
+#endif
+#ifndef KMB_TMA_PRODUCER
+#define KMB_TMA_PRODUCER 1
+#endif
+// a ninth (producer) warp issues the loads instead of warp 0's lane 0:
+// 0 none, 1 real x real, 2 every real-factor product, 3 all
+template <bool CL, bool CU>
+constexpr bool producer_warp() {
+  return KMB_TMA_PRODUCER == 3 || (KMB_TMA_PRODUCER == 2 && !CL) || (KMB_TMA_PRODUCER == 1 && !CL && !CU);
+}
+template <bool CL, bool CU>
+constexpr int threads_for() { return THREADS + (producer_warp<CL, CU>() ? 32 : 0); }
 
 __device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 
@@ -126,16 +143,19 @@ struct StreamK {
 };
 
 // CL = false: real factor (e.g. the Hermite Φ), 2 DMMA per complex multiply-add.
-// Its box is (16 real k, 64 rows) in 128-B rows; one LDS.128 fetches the
-// factor values of two consecutive k-steps (k = 2c, 2c+1 share a 16-B chunk
-// under the k permutation above; 2-way bank conflicts on these reads, which the
-// DMMA rate leaves 4x headroom for).
+// Its box is (8 real k, 64 rows, 2 k halves) in 64-B rows with the 64-B swizzle
+// (16-B chunk ^= (row / 2) % 4); one LDS.128 fetches the factor values of two
+// consecutive k-steps (k = 2c, 2c+1 share a 16-B chunk under the k permutation
+// above).  The 8 lanes of an LDS.128 phase read rows 2q, 2q+1 of one 128-B line,
+// one per 64-B half, so the reads are conflict free (with 128-B rows of 16 k and
+// the 128-B swizzle they were 2-way conflicted: ncu counted 1/3 of the shared
+// wavefronts of a real x real product as conflicts).  KMB_TMA_SW64=0 restores that layout.
 // CU = false: real tensor (e.g. the f64 pipe-flow state).  Fiber-contiguous
 // boxes are (16 fibers, 16 k, 8 fiber groups) in 128-B rows and read with one
-// conflict-free LDS.64 per MMA tile; k-contiguous boxes are (16 k, 128 fibers)
-// and read in k pairs with LDS.128 like the real factor.
+// conflict-free LDS.64 per MMA tile; k-contiguous boxes are (8 k, 128 fibers,
+// 2 k halves) and read in k pairs with LDS.128 like the real factor.
 template <bool KC, int OPK, bool CL = true, bool CU = true, bool SKT = false>
-__global__ void __launch_bounds__(tma::THREADS, 1)
+__global__ void __launch_bounds__(tma::threads_for<CL, CU>(), 1)
     mumode_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                       typename El<double, CU || CL>::T* __restrict__ out, int64_t M, int N, int K, int64_t nl,
                       const OpDev op, const Split sp, const StreamK sk) {
@@ -200,7 +220,10 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
     tma::mbar_expect_tx(&full[s], (CU ? A_BYTES : A_BYTES / 2) + (CL ? B_BYTES : B_BYTES / 2));
     const int k0 = kt * BKS;
     if constexpr (KC && !CU) {
-      tma::load3(st, &mapA, &full[s], k0, static_cast<int>(m0), 0);
+      if constexpr (KMB_TMA_SW64)
+        tma::load3(st, &mapA, &full[s], 0, static_cast<int>(m0), k0 / 8);
+      else
+        tma::load3(st, &mapA, &full[s], k0, static_cast<int>(m0), 0);
     } else if constexpr (!CU) {
       const int kb = k0 / sp.kcb;
       tma::load5(st, &mapA, &full[s], 0, k0 - kb * sp.kcb, a_grp, a_slab, kb);
@@ -210,13 +233,25 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
       const int kb = k0 / sp.kcb;
       tma::load5(st, &mapA, &full[s], 0, k0 - kb * sp.kcb, a_grp, a_slab, kb);
     }
-    if constexpr (CL)
+    if constexpr (CL || KMB_TMA_SW64)
       tma::load3(st + A_BYTES, &mapB, &full[s], 0, n0, k0 / 8);
     else
       tma::load3(st + A_BYTES, &mapB, &full[s], k0, n0, 0);
   };
-  const bool leader = (warp == 0 && lane == 0);
-  if (leader) {
+  constexpr bool PW = tma::producer_warp<CL, CU>();
+  const bool leader = !PW && warp == 0 && lane == 0;
+  if constexpr (PW) {
+    // the producer warp walks the whole ring: a stage is refilled as soon as
+    // all consumers have released it
+    if (warp == CONSUMERS) {
+      if (lane == 0) {
+        tma::prefetch_map(&mapA);
+        tma::prefetch_map(&mapB);
+        for (int64_t q = 0; q < total; ++q) issue(q);
+      }
+      return;
+    }
+  } else if (leader) {
     tma::prefetch_map(&mapA);
     tma::prefetch_map(&mapB);
     for (int64_t q = 0; q < AHEAD && q < total; ++q) issue(q);
@@ -247,7 +282,7 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
       for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
 
     for (int kt = k0; kt < k1; ++kt, ++q) {
-      if (leader && q + AHEAD < total) issue(q + AHEAD);
+      if (!PW && leader && q + AHEAD < total) issue(q + AHEAD);
       const int s = static_cast<int>(q % TSTAGES);
       tma::mbar_wait(&full[s], static_cast<unsigned>((q / TSTAGES) & 1));
       const unsigned st = sbase + s * STAGE_BYTES;
@@ -260,11 +295,13 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 4; ++i) a[i] = tma::lds128(st + ao + i * A_I);
         } else if constexpr (KC) {
-          // real, k-contiguous: row f = wm + 8i + g holds k 0..15; one LDS.128 per k pair
+          // real, k-contiguous: row f = wm + 8i + g of k half ks/2; one LDS.128 per k pair
           if ((ks & 1) == 0) {
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              areal[i] = tma::lds128(st + (wm + i * 8 + g) * 128 + ((((ks >> 1) * 4 + t) ^ g) << 4));
+              areal[i] = KMB_TMA_SW64
+                             ? tma::lds128(st + (ks >> 1) * (BM * 64) + (wm + i * 8 + g) * 64 + ((t ^ (g >> 1)) << 4))
+                             : tma::lds128(st + (wm + i * 8 + g) * 128 + ((((ks >> 1) * 4 + t) ^ g) << 4));
           }
 #pragma unroll
           for (int i = 0; i < 4; ++i) a[i] = make_double2((ks & 1) ? areal[i].y : areal[i].x, 0.0);
@@ -308,10 +345,13 @@ __global__ void __launch_bounds__(tma::THREADS, 1)
           }
         } else {
           if ((ks & 1) == 0) {
-            // row n = wn + 8j + g holds k = 0..15; chunk (k/2) ^ (n % 8), k/2 = (ks/2)*4 + t
+            // row n = wn + 8j + g of k half ks/2 holds k 8(ks/2) .. +7; chunk t ^ (n/2 % 4) holds k pair 2t, 2t+1
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              breal[j] = tma::lds128(st + A_BYTES + (wn + j * 8 + g) * 128 + ((((ks >> 1) * 4 + t) ^ g) << 4));
+              breal[j] = KMB_TMA_SW64 ? tma::lds128(st + A_BYTES + (ks >> 1) * (BN * 64) + (wn + j * 8 + g) * 64 +
+                                                    ((t ^ (g >> 1)) << 4))
+                                      : tma::lds128(st + A_BYTES + (wn + j * 8 + g) * 128 +
+                                                    ((((ks >> 1) * 4 + t) ^ g) << 4));
           }
 #pragma unroll
           for (int i = 0; i < 4; ++i)
