@@ -124,6 +124,7 @@ class DevicePropagatorCache(PropagatorCache):
     def __init__(self, tau, dev_exps):
         object.__setattr__(self, "tau", tau)
         object.__setattr__(self, "_device", {})
+        object.__setattr__(self, "_plans", {})  # kron.step's prebuilt calls (PropagatorCache._plans)
         object.__setattr__(self, "_dev_exps", tuple(dev_exps))
         object.__setattr__(self, "_host", None)
 

@@ -55,3 +55,24 @@ def test_device_cache_step_matches_host_cache():
     dev = km.step(prepare_device(op, 0.01), u)
     assert orc.rel_l2(dev, host) <= 1e-13
     assert prepare_device(op, 0.01).exps[0].shape == (n, n)
+
+
+def test_device_cache_step_with_device_tensor():
+    """A device-resident state through a DevicePropagatorCache takes kron.step's prebuilt-call
+    path (the cache's memo of StepPlans), as the Magnus driver does with device tensors."""
+    n = 64
+    d2 = km.heat_factors(n, 2).factors[0]
+    op = km.KroneckerOp((1j * d2,) * 3)
+    rng = np.random.default_rng(2)
+    u = np.asfortranarray(rng.standard_normal((n,) * 3) + 1j * rng.standard_normal((n,) * 3))
+    cache = prepare_device(op, 0.01)
+    t = dv.to_device(u, np.complex128, dv.device())
+    for _ in range(2):  # the second call reuses the memoised plan
+        got = km.step(cache, t)
+    want = orc.step(km.prepare(op, 0.01).exps, u)
+    assert orc.rel_l2(dv.to_host(got), want) <= 1e-13
+    basis = km.hermite_basis(8)
+    c0 = dv.to_device(np.asfortranarray(golden("hermite")["hkmp8__c0"]), np.complex128, dv.device())
+    c = km.magnus_midpoint_step(lambda s: hkmp_factors(basis, s), c0, 0.0, 0.125, device_expm=True)
+    ref = km.magnus_midpoint_step(lambda s: hkmp_factors(basis, s), golden("hermite")["hkmp8__c0"], 0.0, 0.125)
+    assert orc.rel_l2(dv.to_host(c), ref) <= 1e-12
