@@ -238,9 +238,14 @@ def _fast_tucker(u, mats, pre, post, out_dtype, keepalive):
 
 class StepPlan:
     """A fully prebuilt ``km_tucker`` call for fixed device factors (a PropagatorCache's):
-    ctypes arrays, workspace size, output shape and dtype, and one reusable scratch buffer per
-    stream (calls on one stream are ordered, so consecutive steps may share it).  The hot
-    loop of small states calls ``run`` and nothing else (kron.step's fast path)."""
+    ctypes arrays, workspace size, output shape and dtype, and, for small states, one reusable
+    scratch buffer per stream (calls on one stream are ordered, so consecutive steps may share
+    it).  The hot loop of small states calls ``run`` and nothing else (kron.step's fast path).
+    Scratch above ``KEEP_WS_BYTES`` is taken from torch's allocator per call instead, so a cache
+    kept alive does not pin a state-sized buffer (and a new cache per step, as in the Magnus
+    driver, does not allocate one per step)."""
+
+    KEEP_WS_BYTES = 32 << 20
 
     __slots__ = ("mats", "plan", "c_mats", "ws", "dev")
 
@@ -268,7 +273,11 @@ class StepPlan:
         stream = dv.stream_ptr(dev)
         out = dv.fortran_empty(out_shape, cdt_t, dev)
         ws0 = ws1 = None
-        if need:
+        if need > self.KEEP_WS_BYTES:
+            ws0 = dv.torch.empty(need, dtype=dv.torch.uint8, device=dev)
+            if nact > 1 and not fits:
+                ws1 = dv.torch.empty(need, dtype=dv.torch.uint8, device=dev)
+        elif need:
             bufs = self.ws.get(stream.value)
             if bufs is None:
                 n1 = 2 if (nact > 1 and not fits) else 1

@@ -84,3 +84,29 @@ def test_step_plan_reuse_across_streams_and_dtypes():
     r = km.step(cache, t32)
     assert dv.np_dtype(r.dtype) == np.complex128
     assert orc.rel_l2(dv.to_host(r), orc.step(cache.exps, u.real.astype(np.float32))) <= 1e-12
+
+
+def test_step_plan_does_not_pin_large_scratch():
+    """A state whose Tucker scratch exceeds StepPlan.KEEP_WS_BYTES takes it from torch's allocator
+    per call: the cache keeps no state-sized buffer alive, and the result is unchanged."""
+    import numpy as np
+    import torch
+
+    import paper_2103_01691_b200 as km
+    from oracle import kronmode_oracle as orc
+    from paper_2103_01691_b200 import _device as dv
+    from paper_2103_01691_b200.tensor import StepPlan
+
+    dev = torch.device("cuda", 0)
+    n = 160  # 160^3 complex128: 65.5 MB of scratch
+    rng = np.random.default_rng(13)
+    u = np.asfortranarray(rng.standard_normal((n,) * 3) + 1j * rng.standard_normal((n,) * 3))
+    d2 = km.heat_factors(n, 2).factors[0]
+    cache = km.prepare(km.KroneckerOp((1j * d2,) * 3), 0.01)
+    t = dv.to_device(u, np.complex128, dev)
+    a = km.step(cache, t)
+    b = km.step(cache, t)
+    (plan,) = cache._plans.values()
+    assert plan.ok and plan.plan[7] > StepPlan.KEEP_WS_BYTES and not plan.ws
+    assert torch.equal(a, b)
+    assert orc.rel_l2(dv.to_host(a), orc.step(cache.exps, u)) <= 1e-12

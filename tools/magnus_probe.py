@@ -41,3 +41,30 @@ print("tucker step with device cache: %.3f %.3f" % ev_time(lambda: km.step(cache
 print("prepare_device (3 expm): %.3f %.3f" % ev_time(lambda: prepare_device(op, tau)))
 print("full magnus step: %.3f %.3f" % ev_time(
     lambda: km.magnus_midpoint_step(lambda t: hkmp_factors(b, t), u, 0.1, tau, device_expm=True)))
+from paper_2103_01691_b200 import tensor as _tensor  # noqa: E402
+from paper_2103_01691_b200.kron import _cache_mats, _Operand  # noqa: E402
+
+
+def general_path():
+    c = prepare_device(hkmp_factors(b, 0.1 + 0.5 * tau), tau)
+    return _tensor.run_tucker(u, _cache_mats(c, _Operand(u)))
+
+
+print("magnus step through run_tucker (no StepPlan): %.3f %.3f" % ev_time(general_path))
+print("full magnus step again: %.3f %.3f" % ev_time(
+    lambda: km.magnus_midpoint_step(lambda t: hkmp_factors(b, t), u, 0.1, tau, device_expm=True)))
+
+# the bench_configs sequence: 4 chained steps at s * tau (wall clock per step)
+c0 = u
+for label in ("chained, device expm", "chained, device expm (2nd)", "chained, host expm"):
+    dev_flag = "device" in label
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    x = c0
+    times = []
+    for s in range(4):
+        ts = time.perf_counter()
+        x = km.magnus_midpoint_step(lambda t: hkmp_factors(b, t), x, s * tau, tau, device_expm=dev_flag)
+        torch.cuda.synchronize()
+        times.append((time.perf_counter() - ts) * 1e3)
+    print(label, "per step ms:", ["%.2f" % v for v in times])
