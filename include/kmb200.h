@@ -105,7 +105,8 @@ enum km_kernel_policy {
   KM_POLICY_AUTO = 0,
   KM_POLICY_NO_TMA = 1,
   KM_POLICY_NO_STREAMK = 2,
-  KM_POLICY_NO_TC_HALVES = 4  /* complex64 K' in (512, 1024] on the chunked tcgen05 kernel */
+  KM_POLICY_NO_TC_HALVES = 4,  /* complex64 K' in (512, 1024] on the chunked tcgen05 kernel */
+  KM_POLICY_NO_PLANE_FUSION = 8 /* km_tucker: no fused first-two-products launch for small 3-D complex128 planes */
 };
 int km_set_kernel_policy(int policy);
 

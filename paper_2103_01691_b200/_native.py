@@ -22,7 +22,7 @@ MAX_D = 8
 KM_F32, KM_F64, KM_C64, KM_C128 = 0, 1, 2, 3
 KM_OK, KM_EINVAL, KM_ECUDA = 0, 1, 2
 OP_NONE, OP_GPE_PHASE, OP_DIAG = 0, 1, 2
-POLICY_AUTO, POLICY_NO_TMA, POLICY_NO_STREAMK, POLICY_NO_TC_HALVES = 0, 1, 2, 4
+POLICY_AUTO, POLICY_NO_TMA, POLICY_NO_STREAMK, POLICY_NO_TC_HALVES, POLICY_NO_PLANE_FUSION = 0, 1, 2, 4, 8
 
 # every symbol include/kmb200.h declares
 EXPORTS = (
@@ -132,6 +132,19 @@ def _declare(lib):
     lib.km_pointwise.argtypes = [c_vp, c_vp, c_int, c_i64, p_op, c_vp]
     lib.km_pointwise_cast.restype = c_int
     lib.km_pointwise_cast.argtypes = [c_vp, c_int, c_vp, c_int, c_i64, p_op, c_vp]
+
+
+PLANE_EXTENTS = (32, 48, 64)
+
+
+def plane_fused(u_code, dims, mat_codes, rows):
+    """Whether km_tucker runs the first two products of this step as one fused launch
+    (csrc/kmb200_plane.cuh: d = 3 complex128, square complex128 E1/E2, planes of 32/48/64 on
+    each side) under the default kernel policy; launch counts use it."""
+    return (len(dims) == 3 and u_code == KM_C128 and len(mat_codes) == 3 and all(r > 0 for r in rows)
+            and mat_codes[0] == KM_C128 and mat_codes[1] == KM_C128
+            and rows[0] == dims[0] and rows[1] == dims[1]
+            and dims[0] in PLANE_EXTENTS and dims[1] in PLANE_EXTENTS and dims[2] >= 1)
 
 
 def lib():

@@ -1,6 +1,7 @@
 // libkmb200 C ABI (include/kmb200.h): argument checks, dtype dispatch, the
 // standalone pointwise pass and the Tucker/step driver.  Kernels live in
 // kmb200_kernels.cuh; each dtype combination is instantiated in inst_*.cu.
+#include "kmb200_plane.cuh"
 #include "kmb200_launch.cuh"
 
 #include <algorithm>
@@ -16,6 +17,7 @@ namespace kmb {
 extern bool g_tma_disabled;     // inst_tma_c128.cu
 extern bool g_streamk_disabled;  // inst_tma_c128.cu
 extern bool g_tc_halves_disabled;  // inst_tc32_c64.cu
+extern bool g_plane_disabled;      // inst_plane.cu
 size_t tc32_workspace_bytes(int64_t m, int64_t K);  // inst_tc32_c64.cu
 size_t streamk_workspace_bytes();                    // inst_tma_c128.cu
 int bind_streamk_workspace(cudaStream_t st, void* ws, size_t bytes);  // inst_tma_c128.cu
@@ -344,11 +346,13 @@ extern "C" {
 int km_abi_version(void) { return KMB200_ABI_VERSION; }
 
 int km_set_kernel_policy(int policy) {
-  if (policy < 0 || policy > (KM_POLICY_NO_TMA | KM_POLICY_NO_STREAMK | KM_POLICY_NO_TC_HALVES))
+  if (policy < 0 ||
+      policy > (KM_POLICY_NO_TMA | KM_POLICY_NO_STREAMK | KM_POLICY_NO_TC_HALVES | KM_POLICY_NO_PLANE_FUSION))
     return fail(KM_EINVAL, "km_set_kernel_policy: unknown policy %d", policy);
   g_tma_disabled = (policy & KM_POLICY_NO_TMA) != 0;
   g_streamk_disabled = (policy & KM_POLICY_NO_STREAMK) != 0;
   g_tc_halves_disabled = (policy & KM_POLICY_NO_TC_HALVES) != 0;
+  g_plane_disabled = (policy & KM_POLICY_NO_PLANE_FUSION) != 0;
   return KM_OK;
 }
 
@@ -540,7 +544,18 @@ int km_tucker(const void* u, int u_dtype, int d, const int64_t* dims, const void
     src = pd;
   }
   int dt = u_dtype;
-  for (int a = 0; a < na; ++a) {
+  int a0 = 0;
+  if (d == 3 && na == 3 && u_dtype == KM_C128 && mat_dtypes[0] == KM_C128 && mat_dtypes[1] == KM_C128 &&
+      rows[0] == dims[0] && rows[1] == dims[1]) {
+    // small planes: the first two products fused per i3-plane (kmb200_plane.cuh)
+    rc = launch_plane12(src, mats[0], mats[1], dst[1], dims[0], dims[1], dims[2], st);
+    if (rc > 0) return rc;
+    if (rc == KM_OK) {
+      a0 = 2;
+      src = dst[1];
+    }
+  }
+  for (int a = a0; a < na; ++a) {
     const int mu = active[a];
     int64_t nl = 1, nr = 1;
     for (int i = 0; i < mu; ++i) nl *= cur[i];

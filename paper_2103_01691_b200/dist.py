@@ -37,7 +37,8 @@ class LocalStepper:
         self._c_codes = (ctypes.c_int * self.d)(*[dv.code(dv.np_dtype(m.dtype)) for m in self.mats])
         self._c_rows = (ctypes.c_int64 * self.d)(*[m.shape[0] for m in self.mats])
         self.pre, self.post = pre, post
-        self.launches_per_step = self.d + (1 if pre is not None else 0)
+        self.launches_per_step = self.d + (1 if pre is not None else 0) - \
+            (1 if _native.plane_fused(self.code, self.dims, list(self._c_codes), list(self._c_rows)) else 0)
         self.lib = _native.lib()
 
     def step(self):

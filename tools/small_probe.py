@@ -52,10 +52,23 @@ if __name__ == "__main__":
             st.step()
         torch.cuda.synchronize()
         sys.exit(0)
+    from paper_2103_01691_b200 import _native
+
+    lib = _native.lib()
     for n in (32, 48, 64, 96, 128):
-        st = stepper(n)
-        ms = graph_ms(st)
-        flop = 8 * 3 * n**4 * 10
-        per_launch = [round(x * 1e3, 2) for x in st.time_launches(50)]
-        print(f"n={n}: 10 steps {ms*1e3:.1f} us ({ms*100:.2f} us/step), {flop/ms/1e9:.2f} TFLOP/s; "
-              f"eager per-launch us {per_launch}")
+        res = {}
+        for name, pol in (("fused planes", _native.POLICY_AUTO), ("per product", _native.POLICY_NO_PLANE_FUSION)):
+            _native.check(lib.km_set_kernel_policy(pol))
+            st = stepper(n)
+            ms = graph_ms(st)
+            flop = 8 * 3 * n**4 * 10
+            per_launch = [round(x * 1e3, 2) for x in st.time_launches(50)]
+            st2 = stepper(n)
+            for _ in range(10):
+                st2.step()
+            res[name] = dv.to_host(st2.a)
+            print(f"n={n} {name}: 10 steps {ms*1e3:.1f} us ({ms*100:.2f} us/step), {flop/ms/1e9:.2f} TFLOP/s; "
+                  f"eager per-launch us {per_launch}", flush=True)
+        a, b = res["fused planes"], res["per product"]
+        print(f"   fused vs per-product after 10 steps: rel l2 {np.linalg.norm(a - b) / np.linalg.norm(b):.2e}")
+    _native.check(lib.km_set_kernel_policy(_native.POLICY_AUTO))
