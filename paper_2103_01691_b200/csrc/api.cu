@@ -535,9 +535,18 @@ int km_tucker(const void* u, int u_dtype, int d, const int64_t* dims, const void
     if (dst[a] == out && dst_bytes[a] > out_bytes)
       return fail(KM_EINVAL, "km_tucker: intermediate %d does not fit in out; pass ws1", a + 1);
   }
+  // small planes: the first two products fused per i3-plane (kmb200_plane.cuh).  The
+  // fused launch writes dst[1] (ws0), so a pre-pass must not land there: it takes alt
+  // (ws1 or out; out is read by the fused launch before the last product writes it).
+  const bool fuse = d == 3 && na == 3 && u_dtype == KM_C128 && mat_dtypes[0] == KM_C128 &&
+                    mat_dtypes[1] == KM_C128 && rows[0] == dims[0] && rows[1] == dims[1] &&
+                    plane12_supported(dims[0], dims[1], dims[2]) &&
+                    !((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(mats[0]) |
+                       reinterpret_cast<uintptr_t>(mats[1]) | reinterpret_cast<uintptr_t>(ws0) |
+                       reinterpret_cast<uintptr_t>(alt)) & 15);
   const void* src = u;
   if (has_pre) {
-    void* pd = (dst[0] == ws0) ? alt : ws0;
+    void* pd = fuse ? alt : (dst[0] == ws0) ? alt : ws0;
     if (pd == out && static_cast<size_t>(n_in) * elem_bytes(u_dtype) > out_bytes)
       return fail(KM_EINVAL, "km_tucker: the pre-pass does not fit in out; pass ws1");
     if ((rc = pointwise_impl(u, pd, u_dtype, n_in, pre, st))) return rc;
@@ -545,15 +554,10 @@ int km_tucker(const void* u, int u_dtype, int d, const int64_t* dims, const void
   }
   int dt = u_dtype;
   int a0 = 0;
-  if (d == 3 && na == 3 && u_dtype == KM_C128 && mat_dtypes[0] == KM_C128 && mat_dtypes[1] == KM_C128 &&
-      rows[0] == dims[0] && rows[1] == dims[1]) {
-    // small planes: the first two products fused per i3-plane (kmb200_plane.cuh)
-    rc = launch_plane12(src, mats[0], mats[1], dst[1], dims[0], dims[1], dims[2], st);
-    if (rc > 0) return rc;
-    if (rc == KM_OK) {
-      a0 = 2;
-      src = dst[1];
-    }
+  if (fuse) {
+    if ((rc = launch_plane12(src, mats[0], mats[1], dst[1], dims[0], dims[1], dims[2], st))) return rc;
+    a0 = 2;
+    src = dst[1];
   }
   for (int a = a0; a < na; ++a) {
     const int mu = active[a];

@@ -7,21 +7,27 @@ bool g_plane_disabled = false;  // KM_POLICY_NO_PLANE_FUSION
 
 namespace {
 
-template <int N1, int N2>
-int launch_n(const void* u, const void* E1, const void* E2, void* out, int64_t n3, cudaStream_t st) {
-  // rows per CTA: the most CTAs that still fit one wave and the shared memory
+bool extent_ok(int64_t n) { return n == 32 || n == 48 || n == 64; }
+
+// rows per CTA: the most CTAs that still fit one wave and the shared memory (0: none fits)
+int choose_split(int64_t n1, int64_t n2, int64_t n3) {
   const int64_t S = num_sms();
   int split = 0;
   for (int s = 4; s >= 1; --s) {
-    if (N1 % (16 * s) != 0 || plane12_smem(N1 / s, N2) > 227 * 1024) continue;
+    if (n1 % (16 * s) != 0 || plane12_smem(static_cast<int>(n1) / s, static_cast<int>(n2)) > 227 * 1024) continue;
     if (n3 * s <= S || split == 0) split = s;
     if (n3 * s <= S) break;
   }
-  if (split == 0) return -1;
+  return (n3 * split > 0x7fffffffLL) ? 0 : split;
+}
+
+template <int N1, int N2>
+int launch_n(const void* u, const void* E1, const void* E2, void* out, int64_t n3, cudaStream_t st) {
+  const int split = choose_split(N1, N2, n3);
+  if (split == 0) return fail(KM_EINVAL, "mumode_plane12_kernel: no row split fits");
   auto kern = mumode_plane12_kernel<N1, N2>;
   const int smem = plane12_smem(N1 / split, N2);
   if (int rc = ensure_smem(reinterpret_cast<const void*>(kern), smem, "mumode_plane12_kernel")) return rc;
-  if (n3 * split > 0x7fffffffLL) return -1;
   const cudaError_t e = launch_pdl(kern, dim3(static_cast<unsigned>(n3 * split)), dim3(plane::THREADS), smem, st,
                                    static_cast<const double2*>(u), static_cast<const double2*>(E1),
                                    static_cast<const double2*>(E2), static_cast<double2*>(out), split);
@@ -35,23 +41,27 @@ int launch_n1(const void* u, const void* E1, const void* E2, void* out, int64_t 
     case 32: return launch_n<N1, 32>(u, E1, E2, out, n3, st);
     case 48: return launch_n<N1, 48>(u, E1, E2, out, n3, st);
     case 64: return launch_n<N1, 64>(u, E1, E2, out, n3, st);
-    default: return -1;
+    default: return fail(KM_EINVAL, "mumode_plane12_kernel: n2 = %lld", static_cast<long long>(n2));
   }
 }
 
 }  // namespace
 
+bool plane12_supported(int64_t n1, int64_t n2, int64_t n3) {
+  return !g_plane_disabled && n3 >= 1 && extent_ok(n1) && extent_ok(n2) && choose_split(n1, n2, n3) > 0;
+}
+
 int launch_plane12(const void* u, const void* E1, const void* E2, void* out, int64_t n1, int64_t n2, int64_t n3,
                    cudaStream_t st) {
-  if (g_plane_disabled || n3 < 1) return -1;
-  if ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(E1) | reinterpret_cast<uintptr_t>(E2) |
-       reinterpret_cast<uintptr_t>(out)) & 15)
-    return -1;
+  if (!plane12_supported(n1, n2, n3) ||
+      ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(E1) | reinterpret_cast<uintptr_t>(E2) |
+        reinterpret_cast<uintptr_t>(out)) & 15))
+    return fail(KM_EINVAL, "mumode_plane12_kernel: unsupported shape or alignment");
   switch (n1) {
     case 32: return launch_n1<32>(u, E1, E2, out, n2, n3, st);
     case 48: return launch_n1<48>(u, E1, E2, out, n2, n3, st);
     case 64: return launch_n1<64>(u, E1, E2, out, n2, n3, st);
-    default: return -1;
+    default: return fail(KM_EINVAL, "mumode_plane12_kernel: n1 = %lld", static_cast<long long>(n1));
   }
 }
 

@@ -152,8 +152,10 @@ __global__ void __launch_bounds__(plane::THREADS, 1)
 // shared bytes of one CTA computing r of the n1 rows
 constexpr int plane12_smem(int r, int n2) { return (2 * n2 + 2 * r) * plane::ROW_BYTES; }
 
-// km_tucker's fused path: returns -1 when the shape is not one this kernel
-// covers (the caller then runs the two products separately)
+// km_tucker's fused path: plane12_supported() says whether the kernel covers the
+// shape under the current policy (n1, n2 in {32, 48, 64} and a row split that fits);
+// launch_plane12 needs 16-B aligned pointers and out != u
+bool plane12_supported(int64_t n1, int64_t n2, int64_t n3);
 int launch_plane12(const void* u, const void* E1, const void* E2, void* out, int64_t n1, int64_t n2, int64_t n3,
                    cudaStream_t st);
 

@@ -104,3 +104,25 @@ def test_plane_fusion_ten_steps_graph_replay():
     for _ in range(10):
         want = orc.step(cache.exps, want)
     assert orc.rel_l2(dv.to_host(st.a), want) <= 1e-12
+
+
+@pytest.mark.parametrize("dims", [(64, 64, 300), (48, 32, 333)])
+def test_plane_fusion_after_a_pre_pass_many_waves(dims):
+    """GPE step on rectangular states with hundreds of planes (several waves of plane CTAs): the
+    opening phase must land in a buffer the fused launch does not write (km_tucker puts it in
+    ws1 / out, the fused launch writes ws0), otherwise a plane's CTAs would overwrite rows another
+    CTA of the same plane has not loaded yet."""
+    rng = np.random.default_rng(sum(dims))
+    factors = []
+    for n in dims:
+        h = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+        factors.append(-0.5j * (h + h.conj().T) / n)
+    cache = km.prepare(km.KroneckerOp(tuple(factors)), 0.1)
+    weights = [0.5 + rng.random(n) for n in dims]
+    psi = _rand(dims, 21) * 0.3
+    t = dv.to_device(psi, np.complex128, dv.device())
+    got, names = kernels_launched(lambda: km.gpe_strang_step(cache, weights, t, 0.1))
+    want = orc.gpe_strang_step(cache.exps, weights, psi, 0.1)
+    assert orc.rel_l2(dv.to_host(got), want) <= 1e-12
+    if names is not None:
+        assert any("mumode_plane12_kernel" in n for n in names)
