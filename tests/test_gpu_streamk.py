@@ -162,3 +162,26 @@ def test_random_large_shapes_vs_oracle(seed):
         want = orc.mu_mode_product(u, mat, mu)
         assert orc.rel_l2(a, want) <= 1e-13, (shape, mu, m)
         assert orc.rel_l2(b, want) <= 1e-13, (shape, mu, m)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_large_real_shapes_vs_oracle(seed):
+    """As above for real tensors with real or complex factors (the 64-B-swizzled real tiles, the
+    real x real producer warp): k extents with a half k-block tail (K % 16 == 8), ragged factor
+    row counts, every direction, stream-K and whole tiles."""
+    rng = np.random.default_rng(200 + seed)
+    n1 = int(rng.choice([128, 256]))
+    shape = (n1, int(rng.integers(5, 38)) * 8, int(rng.integers(5, 25)) * 8)
+    u = np.asfortranarray(rng.standard_normal(shape))
+    t = dev(u)
+    for mu in (1, 2, 3):
+        n = shape[mu - 1]
+        m = int(rng.integers(n // 2, n + 40))
+        mat = rng.standard_normal((m, n))
+        if seed % 3 == 2:
+            mat = mat + 1j * rng.standard_normal((m, n))
+        a, b = policies(lambda: dv.to_host(km.mu_mode_product(t, mat, mu)))
+        want = orc.mu_mode_product(u, mat, mu)
+        assert orc.rel_l2(a, want) <= 1e-13, (shape, mu, m)
+        assert orc.rel_l2(b, want) <= 1e-13, (shape, mu, m)
+        assert orc.rel_l2(a, b) <= 1e-14, (shape, mu, m)
