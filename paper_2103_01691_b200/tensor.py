@@ -144,6 +144,10 @@ def _tensor_on_device(op, dtype, dev):
 
 
 _TC_WORKSPACE = {}
+_RR32_ON_TC = True  # float32 x float32 fiber pairs on tcgen05 (False: DMMA; for A/B probes)
+# below this many elements the DMMA route wins (tools/f32_probe.py: 128^3 90 against 130 us,
+# 256^3 1174 against 468 us per step)
+_RR32_MIN_ELEMENTS = 1 << 23
 
 
 def launch_product(src_ptr, src_code, mat_ptr, mat_code, dst_ptr, m, nl, nmu, nr, op, stream, dev):
@@ -320,9 +324,10 @@ def _make_plan(u, mats, pre, post, out_dtype):
     out_shape = tuple(cur)
     if any(n == 0 for n in u.shape) or any(n == 0 for n in out_shape):
         return False
-    if udt == np.dtype(np.complex64) and pre is None and post is None and \
-            all(c == _native.KM_C64 for m, c in zip(mats, codes) if m is not None):
-        return False  # the tcgen05 loop (per-product launches) of the general path
+    for tdt, tcode in ((np.dtype(np.complex64), _native.KM_C64), (np.dtype(np.float32), _native.KM_F32)):
+        if udt == tdt and pre is None and post is None and \
+                all(c == tcode for m, c in zip(mats, codes) if m is not None):
+            return False  # the tcgen05 loop (per-product launches) of the general path
     c_dims = (ctypes.c_int64 * d)(*u.shape)
     c_codes = (ctypes.c_int * d)(*codes)
     c_rows = (ctypes.c_int64 * d)(*rows)
@@ -411,6 +416,13 @@ def _run_tucker(u, mats, pre=None, post=None, out_dtype=None, keepalive=()):
     c64 = np.dtype(np.complex64)
     tc_loop = (u_dt == c64 and pre is None and post is None
                and all(c == _native.KM_C64 for t, c in zip(mats_dev, codes) if t is not None))
+    # float32 x float32 on large states: products whose fibers come in pairs (n_left even) run on
+    # the tcgen05 kernel too, two real fibers read as one complex64 fiber (E z = E u_f + i E u_f+1,
+    # exact) against the factor widened to complex64; direction 1 (n_left = 1) stays on DMMA
+    rr32 = (_RR32_ON_TC and u_dt == np.dtype(np.float32) and pre is None and post is None
+            and prod(uo.shape) >= _RR32_MIN_ELEMENTS
+            and all(c == _native.KM_F32 for t, c in zip(mats_dev, codes) if t is not None))
+    tc_loop = tc_loop or rr32
     if d <= _native.MAX_D and not tc_loop:
         c_dims = (ctypes.c_int64 * d)(*uo.shape)
         c_mats = (ctypes.c_void_p * d)(*[None if t is None else t.data_ptr() for t in mats_dev])
@@ -447,8 +459,14 @@ def _run_tucker(u, mats, pre=None, post=None, out_dtype=None, keepalive=()):
             shape_new = list(shape)
             shape_new[mu] = rows[mu]
             dst = out if idx == len(active) - 1 else dv.fortran_empty(shape_new, dv.torch_dtype(new_dt), dev)
-            launch_product(src.data_ptr(), dv.code(src_dt), mats_dev[mu].data_ptr(), codes[mu], dst.data_ptr(),
-                           rows[mu], prod(shape[:mu]), shape[mu], prod(shape[mu + 1:]), None, stream, dev)
+            nl = prod(shape[:mu])
+            if rr32 and nl % 2 == 0:
+                launch_product(src.data_ptr(), _native.KM_C64, dv.cached_vector(mos[mu].obj, c64, dev).data_ptr(),
+                               _native.KM_C64, dst.data_ptr(), rows[mu], nl // 2, shape[mu], prod(shape[mu + 1:]),
+                               None, stream, dev)
+            else:
+                launch_product(src.data_ptr(), dv.code(src_dt), mats_dev[mu].data_ptr(), codes[mu], dst.data_ptr(),
+                               rows[mu], nl, shape[mu], prod(shape[mu + 1:]), None, stream, dev)
             src, src_dt, shape = dst, new_dt, shape_new
     return _finish(uo, out, result, cdt)
 

@@ -105,3 +105,25 @@ def test_complex64_state_with_real_float32_factor_on_tcgen05(mu):
     assert got.dtype == np.complex64
     want = orc.mu_mode_product(u, phi, mu)
     assert orc.rel_l2(got, want) <= 1e-5
+
+
+@pytest.mark.parametrize("shape", [(256, 256, 128), (160, 256, 256), (2, 4200, 1000), (4096, 2048)])
+def test_float32_products_pair_fibers_on_tcgen05(shape):
+    """float32 x float32: directions with an even n_left read two real fibers as one complex64
+    fiber on the tcgen05 kernel (direction 1 stays on DMMA); parity with the reference's float32
+    arithmetic within the single-precision bar, and the tcgen05 kernel actually ran."""
+    from conftest import kernels_launched
+    from paper_2103_01691_b200 import _device as dv
+
+    rng = np.random.default_rng(sum(shape))
+    u = np.asfortranarray(rng.standard_normal(shape).astype(np.float32))
+    mats = [(rng.standard_normal((n, n)) / np.sqrt(n)).astype(np.float32) for n in shape]
+    t = dv.to_device(u, np.float32, dv.device())
+    got, names = kernels_launched(lambda: km.tucker(t, mats))
+    assert dv.np_dtype(got.dtype) == np.float32
+    want = orc.tucker(u.astype(np.float64), [m.astype(np.float64) for m in mats])
+    assert orc.rel_l2(dv.to_host(got), want) <= 1e-5
+    if names is not None:
+        assert any("mumode_tc32" in n for n in names)
+    host = km.tucker(u, mats)  # numpy in, numpy out (the host pipeline or the same loop)
+    assert host.dtype == np.float32 and orc.rel_l2(host, want) <= 1e-5
