@@ -357,7 +357,13 @@ int km_set_kernel_policy(int policy) {
 }
 
 const char* km_build_info(void) {
-  return "libkmb200 sm_100a: DMMA.8x8x4 mu-mode GEMM (cp.async 3-stage, 128x64 / 64x32 tiles), fused phase epilogue";
+  return "libkmb200 sm_100a: mumode_tma_kernel (TMA + mbarrier ring, DMMA.8x8x4, stream-K tail), "
+         "mumode_tc32_kernel (tcgen05 kind::tf32 3xTF32, CTA pairs), mumode_plane12_kernel (fused planes), "
+         "cp.async DMMA kernels, fused phase / norm / accumulate epilogues"
+#ifdef KMB_CHECK
+         "; KMB_CHECK bounds asserts"
+#endif
+      ;
 }
 
 const char* km_last_error(void) { return g_err; }

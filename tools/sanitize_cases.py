@@ -11,6 +11,8 @@ still compute the right numbers under the tool):
   tc32     tcgen05 CTA-pair kernel (K' <= 512), HALVES (K' <= 1024) and the chunked kernel
   peer     km_mumode_peer / km_mumode_split through P=2 virtual slab ranks (both exchanges)
   misc     pointwise phases, km_norm, km_diag_phase_fold
+  plane    the fused first-two-products launch (mumode_plane12_kernel), also after a GPE
+           pre-pass, and float32 x float32 fiber pairs on the tcgen05 kernel
 Sizes are the smallest that still select each kernel (tile-count and K rules in
 inst_tma_c128.cu / inst_tc32_c64.cu).
 """
@@ -152,8 +154,31 @@ def fam_misc(rng):
     check("diag fold + step", dv.to_host(got), orc.tdpot_strang_step(cache.exps, b.nodes, psi, 0.1, 0.02), 1e-12)
 
 
+def fam_plane(rng):
+    for shape in ((64, 64, 8), (48, 32, 5), (32, 64, 3)):
+        u = crand(rng, shape)
+        mats = [crand(rng, (n, n)) / n for n in shape]
+        t = dv.to_device(u, np.complex128, DEV)
+        got = km.tucker(t, [dv.matrix_to_device(m, np.complex128, DEV) for m in mats])
+        check(f"plane fusion {shape}", dv.to_host(got), orc.tucker(u, mats), 1e-12)
+    shape = (64, 64, 6)
+    factors = [-0.5j * (lambda h: h + h.conj().T)(crand(rng, (n, n))) / n for n in shape]
+    cache = km.prepare(km.KroneckerOp(tuple(factors)), 0.1)
+    ws = [rng.random(n) + 0.5 for n in shape]
+    psi = crand(rng, shape) * 0.3
+    got = km.gpe_strang_step(cache, ws, dv.to_device(psi, np.complex128, DEV), 0.1)
+    check("plane fusion after the GPE pre-pass", dv.to_host(got), orc.gpe_strang_step(cache.exps, ws, psi, 0.1), 1e-12)
+    # float32 fiber pairs on the tcgen05 kernel (large-state route)
+    shape = (256, 256, 128)
+    u = np.asfortranarray(rng.standard_normal(shape).astype(np.float32))
+    mats = [(rng.standard_normal((n, n)) / np.sqrt(n)).astype(np.float32) for n in shape]
+    got = km.tucker(dv.to_device(u, np.float32, DEV), mats)
+    check("float32 fiber pairs", dv.to_host(got), orc.tucker(u.astype(np.float64), [m.astype(np.float64) for m in mats]),
+          1e-5)
+
+
 FAMILIES = {"tma": fam_tma, "streamk": fam_streamk, "cpasync": fam_cpasync, "tc32": fam_tc32, "peer": fam_peer,
-            "misc": fam_misc}
+            "misc": fam_misc, "plane": fam_plane}
 
 
 def main():
