@@ -12,7 +12,6 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2103_01691_b200 as km  # noqa: E402
-from paper_2103_01691_b200 import _device as dv  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 dev = torch.device("cuda", 0)

@@ -7,7 +7,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2103_01691_b200 as km  # noqa: E402
-from paper_2103_01691_b200 import _device as dv, _native, dist  # noqa: E402
+from paper_2103_01691_b200 import _device as dv, _native  # noqa: E402
 
 n = 256
 dev = torch.device("cuda", 0)
