@@ -4,7 +4,6 @@ d = 1..4, with and without the accumulate epilogue.  The kernel choice is
 size dependent, so sweeping shapes sweeps the launch rules (cp.async tile sizes, the
 TMA eligibility, stream-K) as well as the edge handling of each kernel."""
 
-
 import numpy as np
 import pytest
 
