@@ -110,3 +110,40 @@ def test_step_plan_does_not_pin_large_scratch():
     assert plan.ok and plan.plan[7] > StepPlan.KEEP_WS_BYTES and not plan.ws
     assert torch.equal(a, b)
     assert orc.rel_l2(dv.to_host(a), orc.step(cache.exps, u)) <= 1e-12
+
+
+def test_long_step_loops_hold_memory_flat():
+    """Hundreds of public-API steps (64^3 fused planes, 128^3 products, a new Magnus cache per
+    step) leave torch's allocated device memory where the first steps put it: no per-call growth
+    from the prebuilt-call memo, the stream workspaces or the factor caches."""
+    import numpy as np
+    import torch
+
+    import paper_2103_01691_b200 as km
+    from paper_2103_01691_b200 import _device as dv
+    from paper_2103_01691_b200.problems import hkmp_factors
+
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(14)
+    for n in (64, 128):
+        d2 = km.heat_factors(n, 2).factors[0]
+        cache = km.prepare(km.KroneckerOp((1j * d2,) * 3), 0.01)
+        u = dv.to_device(np.asfortranarray(rng.standard_normal((n,) * 3) + 0j), np.complex128, dev)
+        for _ in range(5):
+            u = km.step(cache, u)
+        torch.cuda.synchronize()
+        base = torch.cuda.memory_allocated(dev)
+        for _ in range(300):
+            u = km.step(cache, u)
+        torch.cuda.synchronize()
+        assert torch.cuda.memory_allocated(dev) <= base
+    b = km.hermite_basis(32)
+    c = dv.to_device(np.asfortranarray(rng.standard_normal((32,) * 3) + 0j), np.complex128, dev)
+    for s in range(3):
+        c = km.magnus_midpoint_step(lambda t: hkmp_factors(b, t), c, 0.01 * s, 0.01, device_expm=True)
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated(dev)
+    for s in range(100):
+        c = km.magnus_midpoint_step(lambda t: hkmp_factors(b, t), c, 0.01 * s, 0.01, device_expm=True)
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated(dev) <= base
