@@ -295,7 +295,8 @@ def config_sweep(dev):
 
     rng = np.random.default_rng(0)
     out = []
-    # 1: 64^3 c128, 10 exact steps, per-step launches in a CUDA graph
+    # 1: 64^3 c128, 10 exact steps as one LocalStepper.run (km_steps_paired: two steps per three
+    # fused launches) captured in a CUDA graph
     n = 64
     d2 = km.heat_factors(n, 2).factors[0]
     c1 = km.prepare(km.KroneckerOp((1j * d2,) * 3), 0.01)
@@ -309,11 +310,10 @@ def config_sweep(dev):
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
         with torch.cuda.graph(g, stream=s):
-            for _ in range(10):
-                st.step()
+            st.run(10)
     torch.cuda.synchronize()
-    out.append(entry("1: Schrodinger free 64^3 c128, 10 steps (CUDA graph)", dev_ms(g.replay, 50), 10 * 8 * 3 * n**4,
-                     "ms per 10 steps"))
+    out.append(entry(f"1: Schrodinger free 64^3 c128, 10 steps (CUDA graph, {st.launches_for(10)} launches)",
+                     dev_ms(g.replay, 50), 10 * 8 * 3 * n**4, "ms per 10 steps"))
     del g, st
     # 2: pipe flow 1024^2 f64, one exact step
     n = 1024

@@ -274,6 +274,24 @@ int km_steps_small_workspace_bytes(int64_t n1, int64_t n2, int64_t n3, int64_t s
 int km_steps_small(void* state, const void* E1, const void* E2, const void* E3, int64_t n1, int64_t n2,
                    int64_t n3, int64_t steps, void* workspace, size_t workspace_bytes, void* stream);
 
+/*
+ * `steps` exact steps of a complex128 n1 x n2 x n3 state (reference: kron.step,
+ * kron.py:110-121, applied `steps` times) with every two consecutive steps as
+ * three fused launches: the first two products of step s per i3-plane
+ * (mumode_plane12_kernel), the third products of steps s and s+1 together per
+ * block of 32 fibers (mumode_pencil33_kernel: two E3 products on one
+ * shared-memory tile), and the first two products of step s+1 per i3-plane.
+ * Step s+1 therefore applies its directions in the order 3, 1, 2; products
+ * along different directions commute, so the result differs from the
+ * step-by-step order only in rounding.  An odd last step is (1,2) + 3.
+ * E1..E3 row-major complex128 n_mu x n_mu; n1, n2, n3 in {32, 48, 64};
+ * u is read, the result lands in out, ws is one state-sized scratch buffer
+ * (u, out, ws must not alias).  Every launch is an ordinary stream launch, so
+ * the call can be captured into a CUDA graph.
+ */
+int km_steps_paired(const void* u, const void* E1, const void* E2, const void* E3, int64_t n1, int64_t n2,
+                    int64_t n3, int64_t steps, void* out, void* ws, void* stream);
+
 /* bytes each of ws0/ws1 needs for km_tucker with these arguments */
 int km_tucker_workspace(int u_dtype, int d, const int64_t* dims, const void* const* mats,
                         const int* mat_dtypes, const int64_t* rows, size_t* bytes);

@@ -47,6 +47,7 @@ EXPORTS = (
     "km_stream_workspace_bytes",
     "km_steps_small_workspace_bytes",
     "km_steps_small",
+    "km_steps_paired",
     "km_norm_epilogue_slots",
     "km_set_stream_workspace",
 )
@@ -124,6 +125,8 @@ def _declare(lib):
     lib.km_norm_epilogue_slots.argtypes = [c_i64, c_i64]
     lib.km_steps_small.restype = c_int
     lib.km_steps_small.argtypes = [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_sz, c_vp]
+    lib.km_steps_paired.restype = c_int
+    lib.km_steps_paired.argtypes = [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]
     lib.km_stream_workspace_bytes.restype = c_int
     lib.km_stream_workspace_bytes.argtypes = [ctypes.POINTER(c_sz)]
     lib.km_set_stream_workspace.restype = c_int

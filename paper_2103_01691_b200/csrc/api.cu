@@ -406,6 +406,42 @@ int km_mumode_split(const void* u, int u_dtype, const void* L, int L_dtype, void
                      static_cast<cudaStream_t>(stream), &sp);
 }
 
+int km_steps_paired(const void* u, const void* E1, const void* E2, const void* E3, int64_t n1, int64_t n2,
+                    int64_t n3, int64_t steps, void* out, void* ws, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!u || !E1 || !E2 || !E3 || !out || !ws) return fail(KM_EINVAL, "km_steps_paired: NULL pointer");
+  if (steps < 1) return fail(KM_EINVAL, "km_steps_paired: steps must be >= 1");
+  if (out == u || ws == u || ws == out) return fail(KM_EINVAL, "km_steps_paired: u, out and ws must not alias");
+  const int64_t nfib = n1 * n2;
+  // the plane launches need a row split that fits, the pencil launch 32-fiber blocks
+  if (!plane12_shape_ok(n1, n2, n3) || (steps > 1 && !pencil33_supported(nfib, n3))) return fail(KM_EINVAL, "km_steps_paired: extents must be 32, 48 or 64 (got %lld x %lld x %lld)",
+                       static_cast<long long>(n1), static_cast<long long>(n2), static_cast<long long>(n3));
+  // launch list: per two steps (1,2)(3,3)(1,2) -- step s+1 runs 3, 1, 2 -- and a last odd step (1,2)(3)
+  enum { PLANE, PENCIL, DIR3 };
+  const int64_t launches = (steps / 2) * 3 + (steps % 2) * 2;
+  int64_t k = 0;
+  const void* src = u;
+  auto next_dst = [&]() { return ((launches - 1 - k) % 2 == 0) ? out : ws; };
+  for (int64_t s = 0; s < steps; s += 2) {
+    const bool pair = s + 1 < steps;
+    const int kinds[3] = {PLANE, pair ? PENCIL : DIR3, PLANE};
+    for (int i = 0; i < (pair ? 3 : 2); ++i, ++k) {
+      void* dst = next_dst();
+      int rc = KM_OK;
+      if (kinds[i] == PLANE) {
+        rc = launch_plane12(src, E1, E2, dst, n1, n2, n3, st);
+      } else if (kinds[i] == PENCIL) {
+        rc = launch_pencil33(src, E3, E3, dst, nfib, n3, st);
+      } else {
+        rc = mumode_impl(src, KM_C128, E3, KM_C128, dst, n3, nfib, n3, 1, nullptr, st);
+      }
+      if (rc) return rc;
+      src = dst;
+    }
+  }
+  return KM_OK;
+}
+
 int km_steps_small_workspace_bytes(int64_t n1, int64_t n2, int64_t n3, int64_t steps, size_t* bytes) {
   return steps_small_workspace(n1, n2, n3, steps, bytes);
 }

@@ -149,13 +149,95 @@ __global__ void __launch_bounds__(plane::THREADS, 1)
   }
 }
 
+// mumode_pencil33_kernel — two products along the trailing direction of a small
+// complex128 state fused per block of fibers: w = (u ×₃ Ea) ×₃ Eb, i.e. for the
+// F (32, or 16 when that leaves too few CTAs) fibers f0.. of the CTA (fibers =
+// (i1, i2), contiguous in memory)
+//     Y1 = X · Eaᵀ,  Y2 = Y1 · Ebᵀ     (X[f][k] = u(f0 + f, k), k = i3)
+// with X, Ea, Eb and Y1 in shared memory (the layout and warp tiles of the
+// plane kernel).  km_steps_paired runs the third products of two consecutive
+// steps with it (tensor.py:143-166 twice along μ = 3).
+template <int N3, int F>
+__global__ void __launch_bounds__(plane::THREADS, 1)
+    mumode_pencil33_kernel(const double2* __restrict__ u, const double2* __restrict__ Ea,
+                           const double2* __restrict__ Eb, double2* __restrict__ out, int64_t nfib) {
+  using namespace plane;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sX = smem_raw;              // F rows: f, k = i3
+  unsigned char* sY = sX + F * ROW_BYTES;    // F rows: f, k = j (the first product)
+  unsigned char* sA = sY + F * ROW_BYTES;    // N3 rows: Ea
+  unsigned char* sB = sA + N3 * ROW_BYTES;   // N3 rows: Eb (aliases Ea when Eb == Ea)
+  const bool same = (Ea == Eb);
+  if (same) sB = sA;
+  const unsigned aX = su32(sX), aY = su32(sY), aA = su32(sA), aB = su32(sB);
+  const int64_t f0 = static_cast<int64_t>(blockIdx.x) * F;
+
+  pdl_wait();
+  for (int e = threadIdx.x; e < F * N3; e += THREADS) {  // X: F contiguous fibers per k
+    const int k = e / F, f = e - k * F;
+    cp_async<16>(sX + off(f, k), u + f0 + f + k * nfib, true);
+  }
+  for (int e = threadIdx.x; e < N3 * N3; e += THREADS) {  // Ea, row-major
+    const int j = e / N3, k = e - j * N3;
+    cp_async<16>(sA + off(j, k), Ea + e, true);
+  }
+  cp_commit();
+  if (!same) {
+    for (int e = threadIdx.x; e < N3 * N3; e += THREADS) {
+      const int j = e / N3, k = e - j * N3;
+      cp_async<16>(sB + off(j, k), Eb + e, true);
+    }
+  }
+  cp_commit();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  constexpr int TC = N3 / 16, TILES = (F / 16) * TC;
+  cp_wait<1>();
+  __syncthreads();
+  for (int w = warp; w < TILES; w += THREADS / 32) {  // Y1 = X · Eaᵀ
+    const int ra = (w / TC) * 16, cb = (w % TC) * 16;
+    double cr[2][2][2] = {}, ci[2][2][2] = {};
+    warp_tile<N3>(aX, aA, ra, cb, g, t, cr, ci);
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) sts(aY + off(ra + 8 * i + g, cb + 8 * j + 2 * t + h), cr[i][j][h], ci[i][j][h]);
+  }
+  cp_wait<0>();
+  __syncthreads();
+  for (int w = warp; w < TILES; w += THREADS / 32) {  // Y2 = Y1 · Ebᵀ -> out(f0 + f, j)
+    const int ra = (w / TC) * 16, cb = (w % TC) * 16;
+    double cr[2][2][2] = {}, ci[2][2][2] = {};
+    warp_tile<N3>(aY, aB, ra, cb, g, t, cr, ci);
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int f = ra + 8 * i + g, col = cb + 8 * j + 2 * t + h;
+          KMB_ASSERT(f0 + f < nfib && col < N3);
+          out[f0 + f + col * nfib] = make_double2(cr[i][j][h], ci[i][j][h]);
+        }
+  }
+}
+
+constexpr int pencil33_smem(int n3, int f) { return (2 * f + 2 * n3) * plane::ROW_BYTES; }
+
 // shared bytes of one CTA computing r of the n1 rows
 constexpr int plane12_smem(int r, int n2) { return (2 * n2 + 2 * r) * plane::ROW_BYTES; }
 
 // km_tucker's fused path: plane12_supported() says whether the kernel covers the
 // shape under the current policy (n1, n2 in {32, 48, 64} and a row split that fits);
 // launch_plane12 needs 16-B aligned pointers and out != u
-bool plane12_supported(int64_t n1, int64_t n2, int64_t n3);
+bool plane12_supported(int64_t n1, int64_t n2, int64_t n3);  // the shape, and KM_POLICY_NO_PLANE_FUSION unset
+bool plane12_shape_ok(int64_t n1, int64_t n2, int64_t n3);   // the shape alone (km_steps_paired)
+// two trailing-direction products on blocks of 16 or 32 fibers (nfib % 32 == 0, n3 in {32, 48, 64})
+bool pencil33_supported(int64_t nfib, int64_t n3);
+int launch_pencil33(const void* u, const void* Ea, const void* Eb, void* out, int64_t nfib, int64_t n3,
+                    cudaStream_t st);
 int launch_plane12(const void* u, const void* E1, const void* E2, void* out, int64_t n1, int64_t n2, int64_t n3,
                    cudaStream_t st);
 

@@ -51,10 +51,14 @@ class LocalStepper:
             None if self.post is None else ctypes.byref(self.post), stream))
         self.a, self.b = self.b, self.a
 
-    def run(self, steps, persistent=False):
-        """``steps`` exact steps, one ``km_tucker`` launch each.
+    def run(self, steps, persistent=False, paired=None):
+        """``steps`` exact steps.
 
-        ``persistent=True`` runs them instead as ONE launch (``km_steps_small``: the 3·steps
+        Small complex128 cubes (extents 32, 48 or 64, square complex128 factors, no phase ops)
+        take ``km_steps_paired`` by default (``paired=None``): every two steps as three fused
+        launches, (1,2) per i3-plane, the two steps' direction-3 products together per block
+        of fibers, (1,2) again; ``paired=False`` keeps one ``km_tucker``
+        launch per step.  ``persistent=True`` runs them instead as ONE launch (``km_steps_small``: the 3·steps
         sweeps as a dataflow of 32 x 32 tiles with dependency counters) for complex128 3D
         states whose extents are multiples of 32 up to 96.  It is correct and kept for the
         record, but measured slower than the per-step launches replayed as a CUDA graph
@@ -64,6 +68,12 @@ class LocalStepper:
         """
         if steps < 1:
             return
+        if not persistent and paired is not False and self.paired_ok():
+            _native.check(self.lib.km_steps_paired(
+                self.a.data_ptr(), self.mats[0].data_ptr(), self.mats[1].data_ptr(), self.mats[2].data_ptr(),
+                *self.dims, steps, self.b.data_ptr(), self.w.data_ptr(), dv.stream_ptr(self.a.device)))
+            self.a, self.b = self.b, self.a
+            return
         ws = self._steps_workspace(steps) if persistent else None
         if ws is None:
             for _ in range(steps):
@@ -72,6 +82,20 @@ class LocalStepper:
         _native.check(self.lib.km_steps_small(
             self.a.data_ptr(), self.mats[0].data_ptr(), self.mats[1].data_ptr(), self.mats[2].data_ptr(),
             *self.dims, steps, ws.data_ptr(), ws.numel(), dv.stream_ptr(self.a.device)))
+
+    def paired_ok(self):
+        """Whether ``run`` takes ``km_steps_paired`` (its shape and dtype rules)."""
+        torch = self.torch
+        return (self.d == 3 and self.pre is None and self.post is None and self.a.dtype == torch.complex128
+                and dv.is_fortran(self.a) and all(n in _native.PLANE_EXTENTS for n in self.dims)
+                and all(m.dtype == torch.complex128 and tuple(m.shape) == (n, n) and m.is_contiguous()
+                        for m, n in zip(self.mats, self.dims)))
+
+    def launches_for(self, steps):
+        """Launches ``run(steps)`` issues (the bench's ``gpu_launches``)."""
+        if self.paired_ok():
+            return (steps // 2) * 3 + (steps % 2) * 2
+        return steps * self.launches_per_step
 
     def _steps_workspace(self, steps):
         torch = self.torch

@@ -126,3 +126,67 @@ def test_plane_fusion_after_a_pre_pass_many_waves(dims):
     assert orc.rel_l2(dv.to_host(got), want) <= 1e-12
     if names is not None:
         assert any("mumode_plane12_kernel" in n for n in names)
+
+
+@pytest.mark.parametrize("dims,steps", [((64, 64, 64), 10), ((64, 64, 64), 1), ((64, 64, 64), 3),
+                                        ((48, 48, 48), 4), ((32, 64, 48), 5), ((64, 32, 32), 2)])
+def test_steps_paired_matches_oracle_and_per_step(dims, steps):
+    """km_steps_paired (LocalStepper.run): two steps per three fused launches, step s+1 in the
+    direction order 3, 1, 2 -- equal to the step-by-step oracle up to rounding."""
+    from paper_2103_01691_b200 import dist
+
+    u = _rand(dims, sum(dims) + steps)
+    factors = []
+    rng = np.random.default_rng(steps)
+    for n in dims:
+        h = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+        factors.append(-0.5j * (h + h.conj().T) / n)
+    cache = km.prepare(km.KroneckerOp(tuple(factors)), 0.2)
+    mats = cache.device_exps((np.complex128,) * 3, dv.device())
+    st = dist.LocalStepper(dv.to_device(u, np.complex128, dv.device()), mats)
+    assert st.paired_ok() and st.launches_for(steps) == (steps // 2) * 3 + (steps % 2) * 2
+    _, names = kernels_launched(lambda: st.run(steps))
+    ref = dist.LocalStepper(dv.to_device(u, np.complex128, dv.device()), mats)
+    ref.run(steps, paired=False)
+    want = u
+    for _ in range(steps):
+        want = orc.step(cache.exps, want)
+    got = dv.to_host(st.a)
+    assert orc.rel_l2(got, want) <= 1e-13
+    assert orc.rel_l2(got, dv.to_host(ref.a)) <= 1e-14
+    if names is not None:
+        assert any("mumode_plane12_kernel" in n for n in names)
+        assert (steps > 1) == any("mumode_pencil33_kernel" in n for n in names)
+
+
+def test_steps_paired_graph_and_abi_errors():
+    import ctypes
+
+    import torch
+
+    from paper_2103_01691_b200 import dist
+
+    n = 64
+    u = _rand((n,) * 3, 31)
+    d2 = km.heat_factors(n, 2).factors[0]
+    cache = km.prepare(km.KroneckerOp((1j * d2,) * 3), 0.01)
+    mats = cache.device_exps((np.complex128,) * 3, dv.device())
+    st = dist.LocalStepper(dv.to_device(u, np.complex128, dv.device()), mats)
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
+        st.run(10)
+    g.replay()
+    torch.cuda.synchronize()
+    want = u
+    for _ in range(10):
+        want = orc.step(cache.exps, want)
+    assert orc.rel_l2(dv.to_host(st.a), want) <= 1e-12
+    lib = _native.lib()
+    a, b, w = st.a, st.b, st.w
+    p = [ctypes.c_void_p(m.data_ptr()) for m in mats]
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert lib.km_steps_paired(a.data_ptr(), *p, n, n, n, 2, a.data_ptr(), w.data_ptr(), stream) == _native.KM_EINVAL
+    assert lib.km_steps_paired(a.data_ptr(), *p, n, n, 96, 2, b.data_ptr(), w.data_ptr(), stream) == _native.KM_EINVAL
+    assert lib.km_steps_paired(a.data_ptr(), *p, n, n, n, 0, b.data_ptr(), w.data_ptr(), stream) == _native.KM_EINVAL

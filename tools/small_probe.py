@@ -22,7 +22,7 @@ def stepper(n):
     return dist.LocalStepper(dv.to_device(u, np.complex128, DEV), cache.device_exps((np.complex128,) * 3, DEV))
 
 
-def graph_ms(st, steps=10, reps=50):
+def graph_ms(st, steps=10, reps=50, paired=False):
     for _ in range(3):
         st.step()
     torch.cuda.synchronize()
@@ -31,8 +31,11 @@ def graph_ms(st, steps=10, reps=50):
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
         with torch.cuda.graph(g, stream=s):
-            for _ in range(steps):
-                st.step()
+            if paired:
+                st.run(steps)
+            else:
+                for _ in range(steps):
+                    st.step()
     torch.cuda.synchronize()
     for _ in range(3):
         g.replay()
@@ -71,4 +74,13 @@ if __name__ == "__main__":
                   f"eager per-launch us {per_launch}", flush=True)
         a, b = res["fused planes"], res["per product"]
         print(f"   fused vs per-product after 10 steps: rel l2 {np.linalg.norm(a - b) / np.linalg.norm(b):.2e}")
+        st = stepper(n)
+        if st.paired_ok():
+            ms = graph_ms(st, paired=True)
+            st2 = stepper(n)
+            st2.run(10)
+            c = dv.to_host(st2.a)
+            print(f"n={n} paired steps (km_steps_paired, {st.launches_for(10)} launches): 10 steps {ms*1e3:.1f} us "
+                  f"({ms*100:.2f} us/step), {8 * 3 * n**4 * 10 / ms / 1e9:.2f} TFLOP/s; vs per-product rel l2 "
+                  f"{np.linalg.norm(c - b) / np.linalg.norm(b):.2e}", flush=True)
     _native.check(lib.km_set_kernel_policy(_native.POLICY_AUTO))
