@@ -93,6 +93,15 @@ def case_steps():
     return lambda: st.run(10, persistent=True)
 
 
+def case_paired():
+    """64^3 complex128 x 2 steps as km_steps_paired's three fused launches (plane, pencil, plane)."""
+    from paper_2103_01691_b200 import dist
+
+    cache, t = schrod(64), dv.to_device(crand((64,) * 3), np.complex128, DEV)
+    st = dist.LocalStepper(t, cache.device_exps((np.complex128,) * 3, DEV))
+    return lambda: st.run(2)
+
+
 def case_matvec():
     """256^3 complex128 Kronecker-sum matvec: 3 products, the last two accumulating in the epilogue."""
     d2 = km.heat_factors(256, 2).factors[0]
@@ -110,7 +119,8 @@ def case_gpe64():
 
 
 CASES = {"c128": case_c128, "c64": case_c64, "small": case_small, "pipe": case_pipe, "gpe": case_gpe,
-         "norm": case_norm, "slab8": case_slab8, "steps": case_steps, "matvec": case_matvec, "gpe64": case_gpe64}
+         "norm": case_norm, "slab8": case_slab8, "steps": case_steps, "matvec": case_matvec, "gpe64": case_gpe64,
+         "paired": case_paired}
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(CASES)

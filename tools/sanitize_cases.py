@@ -168,6 +168,17 @@ def fam_plane(rng):
     psi = crand(rng, shape) * 0.3
     got = km.gpe_strang_step(cache, ws, dv.to_device(psi, np.complex128, DEV), 0.1)
     check("plane fusion after the GPE pre-pass", dv.to_host(got), orc.gpe_strang_step(cache.exps, ws, psi, 0.1), 1e-12)
+    # two steps in three fused launches (plane, pencil, plane), 32- and 16-fiber pencil blocks
+    from paper_2103_01691_b200 import dist
+
+    for shape in ((64, 64, 64), (48, 48, 48)):
+        factors = [-0.5j * (lambda h: h + h.conj().T)(crand(rng, (n, n))) / n for n in shape]
+        cache = km.prepare(km.KroneckerOp(tuple(factors)), 0.1)
+        u = crand(rng, shape)
+        st = dist.LocalStepper(dv.to_device(u, np.complex128, DEV), cache.device_exps((np.complex128,) * 3, DEV))
+        st.run(3)
+        check(f"paired steps {shape}", dv.to_host(st.a),
+              orc.step(cache.exps, orc.step(cache.exps, orc.step(cache.exps, u))), 1e-12)
     # float32 fiber pairs on the tcgen05 kernel (large-state route)
     shape = (256, 256, 128)
     u = np.asfortranarray(rng.standard_normal(shape).astype(np.float32))
