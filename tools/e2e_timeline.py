@@ -1,6 +1,7 @@
 """Device timeline of one drop-in step(cache, numpy) call (host-pipelined path):
 H2D slabs, per-slab products, direction-d row blocks and D2H blocks, in ms
-from the call's first event.  python tools/e2e_timeline.py"""
+from the call's first event.  python tools/e2e_timeline.py [--pageable]
+(--pageable: an ordinary numpy input, staged through the page-locked ring)"""
 import os
 import sys
 import time
@@ -17,6 +18,10 @@ N = u.shape[0]
 pinned = torch.empty((N, N, N), dtype=torch.complex128, pin_memory=True)
 pinned.numpy()[...] = u.transpose(2, 1, 0)
 host = pinned.numpy().transpose(2, 1, 0)
+if "--pageable" in sys.argv:
+    import numpy as np
+
+    host = np.asfortranarray(u.copy())
 for _ in range(3):
     km.step(cache, host)
 torch.cuda.synchronize()
