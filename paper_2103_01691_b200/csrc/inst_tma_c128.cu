@@ -29,12 +29,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 bool make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
-              const cuuint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+              const cuuint32_t* box) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -195,36 +195,18 @@ int launch_tma_f64(const void* u, const void* L, void* out, int64_t M, int N, in
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(K) * 16, 128};
     cuuint32_t box[3] = {16, tma::BN, 2};
     if (!make_map(&mb, L, 3, dims, strides, box)) return -1;
-  } else {
-#if KMB_TMA_SW64
-    // real factor: dims (8 k, rows, k groups), box (8, 64, 2), 64-B swizzle
-    //   -> smem [k half][row][8 k] (kmb200_tma.cuh: conflict-free k-pair reads)
-    cuuint64_t dims[3] = {8, static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(K / 8)};
-    cuuint64_t strides[2] = {static_cast<cuuint64_t>(K) * 8, 64};
-    cuuint32_t box[3] = {8, tma::BN, 2};
-    if (!make_map(&mb, L, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B)) return -1;
-#else
-    // real factor: dims (k, rows), 128-B rows of 16 k
+  } else {  // real factor: dims (k, rows), 128-B rows of 16 k
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(N), 1};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(K) * 8, static_cast<cuuint64_t>(K) * 8 * N};
     cuuint32_t box[3] = {16, tma::BN, 1};
     if (!make_map(&mb, L, 3, dims, strides, box)) return -1;
-#endif
   }
-  if (kc && !complex_tensor) {
-#if KMB_TMA_SW64
-    // real, k-contiguous: dims (8 k, fibers, k groups), box (8, 128, 2), 64-B swizzle
-    cuuint64_t dims[3] = {8, static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(K / 8)};
-    cuuint64_t strides[2] = {static_cast<cuuint64_t>(K) * 8, 64};
-    cuuint32_t box[3] = {8, tma::BM, 2};
-    if (!make_map(&ma, u, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B)) return -1;
-#else
-    // real, k-contiguous: dims (k, fibers), 128-B rows of 16 k
+  if (kc && !complex_tensor) {  // real, k-contiguous: dims (k, fibers), 128-B rows of 16 k
+    if (K % 2 != 0) return -1;
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M), 1};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(K) * 8, static_cast<cuuint64_t>(K) * 8 * M};
     cuuint32_t box[3] = {16, tma::BM, 1};
     if (!make_map(&ma, u, 3, dims, strides, box)) return -1;
-#endif
   } else if (kc) {  // complex, k-contiguous: dims (16 f64 = 8 complex k, fibers, k groups)
     cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(K / 8)};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(K) * 16, 128};

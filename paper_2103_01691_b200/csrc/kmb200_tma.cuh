@@ -54,9 +54,6 @@ constexpr int THREADS = 32 * CONSUMERS;
 constexpr int AHEAD = KMB_TMA_AHEAD;  // k-blocks between a stage's load and its use
 constexpr int A_BYTES = BM * BKS * 16, B_BYTES = BN * BKS * 16, STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int SMEM_BYTES = TSTAGES * STAGE_BYTES + 2 * TSTAGES * 8 + 1024;
-#ifndef KMB_TMA_SW64
-#define KMB_TMA_SW64 1
-#endif
 #ifndef KMB_TMA_PRODUCER
 #define KMB_TMA_PRODUCER 1
 #endif
@@ -143,17 +140,15 @@ struct StreamK {
 };
 
 // CL = false: real factor (e.g. the Hermite Φ), 2 DMMA per complex multiply-add.
-// Its box is (8 real k, 64 rows, 2 k halves) in 64-B rows with the 64-B swizzle
-// (16-B chunk ^= (row / 2) % 4); one LDS.128 fetches the factor values of two
-// consecutive k-steps (k = 2c, 2c+1 share a 16-B chunk under the k permutation
-// above).  The 8 lanes of an LDS.128 phase read rows 2q, 2q+1 of one 128-B line,
-// one per 64-B half, so the reads are conflict free (with 128-B rows of 16 k and
-// the 128-B swizzle they were 2-way conflicted: ncu counted 1/3 of the shared
-// wavefronts of a real x real product as conflicts).  KMB_TMA_SW64=0 restores that layout.
+// Its box is (16 real k, 64 rows) in 128-B rows; one LDS.128 fetches the
+// factor values of two consecutive k-steps (k = 2c, 2c+1 share a 16-B chunk
+// under the k permutation above; 2-way bank conflicts on these reads, which the
+// DMMA rate leaves room for: a conflict-free 64-B-swizzled layout measured < 1 %
+// faster and was withdrawn).
 // CU = false: real tensor (e.g. the f64 pipe-flow state).  Fiber-contiguous
 // boxes are (16 fibers, 16 k, 8 fiber groups) in 128-B rows and read with one
-// conflict-free LDS.64 per MMA tile; k-contiguous boxes are (8 k, 128 fibers,
-// 2 k halves) and read in k pairs with LDS.128 like the real factor.
+// conflict-free LDS.64 per MMA tile; k-contiguous boxes are (16 k, 128 fibers)
+// and read in k pairs with LDS.128 like the real factor.
 template <bool KC, int OPK, bool CL = true, bool CU = true, bool SKT = false>
 __global__ void __launch_bounds__(tma::threads_for<CL, CU>(), 1)
     mumode_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
@@ -220,10 +215,7 @@ __global__ void __launch_bounds__(tma::threads_for<CL, CU>(), 1)
     tma::mbar_expect_tx(&full[s], (CU ? A_BYTES : A_BYTES / 2) + (CL ? B_BYTES : B_BYTES / 2));
     const int k0 = kt * BKS;
     if constexpr (KC && !CU) {
-      if constexpr (KMB_TMA_SW64)
-        tma::load3(st, &mapA, &full[s], 0, static_cast<int>(m0), k0 / 8);
-      else
-        tma::load3(st, &mapA, &full[s], k0, static_cast<int>(m0), 0);
+      tma::load3(st, &mapA, &full[s], k0, static_cast<int>(m0), 0);
     } else if constexpr (!CU) {
       const int kb = k0 / sp.kcb;
       tma::load5(st, &mapA, &full[s], 0, k0 - kb * sp.kcb, a_grp, a_slab, kb);
@@ -233,7 +225,7 @@ __global__ void __launch_bounds__(tma::threads_for<CL, CU>(), 1)
       const int kb = k0 / sp.kcb;
       tma::load5(st, &mapA, &full[s], 0, k0 - kb * sp.kcb, a_grp, a_slab, kb);
     }
-    if constexpr (CL || KMB_TMA_SW64)
+    if constexpr (CL)
       tma::load3(st + A_BYTES, &mapB, &full[s], 0, n0, k0 / 8);
     else
       tma::load3(st + A_BYTES, &mapB, &full[s], k0, n0, 0);
@@ -295,13 +287,11 @@ __global__ void __launch_bounds__(tma::threads_for<CL, CU>(), 1)
 #pragma unroll
           for (int i = 0; i < 4; ++i) a[i] = tma::lds128(st + ao + i * A_I);
         } else if constexpr (KC) {
-          // real, k-contiguous: row f = wm + 8i + g of k half ks/2; one LDS.128 per k pair
+          // real, k-contiguous: row f = wm + 8i + g holds k 0..15; one LDS.128 per k pair
           if ((ks & 1) == 0) {
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              areal[i] = KMB_TMA_SW64
-                             ? tma::lds128(st + (ks >> 1) * (BM * 64) + (wm + i * 8 + g) * 64 + ((t ^ (g >> 1)) << 4))
-                             : tma::lds128(st + (wm + i * 8 + g) * 128 + ((((ks >> 1) * 4 + t) ^ g) << 4));
+              areal[i] = tma::lds128(st + (wm + i * 8 + g) * 128 + ((((ks >> 1) * 4 + t) ^ g) << 4));
           }
 #pragma unroll
           for (int i = 0; i < 4; ++i) a[i] = make_double2((ks & 1) ? areal[i].y : areal[i].x, 0.0);
@@ -345,13 +335,10 @@ __global__ void __launch_bounds__(tma::threads_for<CL, CU>(), 1)
           }
         } else {
           if ((ks & 1) == 0) {
-            // row n = wn + 8j + g of k half ks/2 holds k 8(ks/2) .. +7; chunk t ^ (n/2 % 4) holds k pair 2t, 2t+1
+            // row n = wn + 8j + g holds k = 0..15; chunk (k/2) ^ (n % 8), k/2 = (ks/2)*4 + t
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              breal[j] = KMB_TMA_SW64 ? tma::lds128(st + A_BYTES + (ks >> 1) * (BN * 64) + (wn + j * 8 + g) * 64 +
-                                                    ((t ^ (g >> 1)) << 4))
-                                      : tma::lds128(st + A_BYTES + (wn + j * 8 + g) * 128 +
-                                                    ((((ks >> 1) * 4 + t) ^ g) << 4));
+              breal[j] = tma::lds128(st + A_BYTES + (wn + j * 8 + g) * 128 + ((((ks >> 1) * 4 + t) ^ g) << 4));
           }
 #pragma unroll
           for (int i = 0; i < 4; ++i)

@@ -185,3 +185,25 @@ def test_random_large_real_shapes_vs_oracle(seed):
         assert orc.rel_l2(a, want) <= 1e-13, (shape, mu, m)
         assert orc.rel_l2(b, want) <= 1e-13, (shape, mu, m)
         assert orc.rel_l2(a, b) <= 1e-14, (shape, mu, m)
+
+
+@pytest.mark.parametrize("policy", ["auto", "whole"])
+def test_repeated_real_products_are_identical(policy):
+    """A real x real k-contiguous product with half-k-block and row tails, launched many times:
+    every launch must give the same, correct result (a randomised sweep once caught a
+    layout / producer-warp combination that went wrong in ~1 of 10 launches)."""
+    rng = np.random.default_rng(216)
+    u = np.asfortranarray(rng.standard_normal((216, 213, 263)))
+    mat = rng.standard_normal((194, 216)) / np.sqrt(216)
+    want = orc.mu_mode_product(u, mat, 1)
+    t = dev(u)
+    lib = _native.lib()
+    try:
+        if policy == "whole":
+            _native.check(lib.km_set_kernel_policy(_native.POLICY_NO_STREAMK))
+        first = dv.to_host(km.mu_mode_product(t, mat, 1))
+        assert orc.rel_l2(first, want) <= 1e-13
+        for _ in range(60):
+            assert np.array_equal(dv.to_host(km.mu_mode_product(t, mat, 1)), first)
+    finally:
+        _native.check(lib.km_set_kernel_policy(_native.POLICY_AUTO))
