@@ -3,6 +3,7 @@ and without the stream-K cut, and parity against the oracle.
 
     python tools/pipe_probe.py [n]
 """
+import gc
 import os
 import sys
 
@@ -33,6 +34,7 @@ for cplx in (False, True):
         for _ in range(3):
             km.step(cache, t)
         torch.cuda.synchronize()
+        gc.collect()  # a collector pause inside the timed loop idles the GPU between launches
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(50):
