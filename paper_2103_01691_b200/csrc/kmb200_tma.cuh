@@ -13,7 +13,7 @@
 //     and caps every thread at 168 registers; the complex accumulators alone
 //     need 128, so only the real x real products, 64 accumulator registers,
 //     use one: there it walks the whole ring and takes the load bookkeeping
-//     off warp 0, which otherwise paces the CTA — 3.4 % on a 512^3 f64
+//     off warp 0, which otherwise paces the CTA — 1.5 % on a 512^3 f64
 //     product, tools/ab_probe.py.)
 //   * the grid is persistent (one CTA per SM) and walks the tiles with a
 //     static stride; the k-block counter runs across tiles, so the loads of
