@@ -5,6 +5,9 @@
 
 namespace kmb {
 
+#ifndef KMB_TC_HALVES_MIN
+#define KMB_TC_HALVES_MIN 512  // K' above which a tile accumulates in two chains
+#endif
 bool g_tc_halves_disabled = false;  // A/B switch (KMB200_TC_HALVES=0): K' in (512, 1024] on the chunked kernel
 
 namespace {
@@ -79,7 +82,7 @@ int launch(const CUtensorMap& ahi, const CUtensorMap& alo, const CUtensorMap& b,
                         "mumode_tc32_chunk_kernel", ahi, alo, b, mo, F, m, K, nl, st);
   }
   const int64_t tiles = ((2 * m + 2 * tc32::BMR - 1) / (2 * tc32::BMR)) * ((fib_r + tc32::BNR - 1) / tc32::BNR);
-  if ((KC ? 2 * K : K) > 512) {  // two accumulation chains of <= 512 k' per tile
+  if ((KC ? 2 * K : K) > KMB_TC_HALVES_MIN) {  // two accumulation chains per tile
     return launch_pairs(mumode_tc32_kernel<KC, true>, tc32::SMEM_BYTES, tc32::THREADS, tiles,
                         "mumode_tc32_kernel (halves)", ahi, alo, b, mo, F, m, K, nl, st);
   }
